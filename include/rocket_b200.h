@@ -1,0 +1,135 @@
+/*
+ * rocket_b200.h — C ABI of the B200-native ROCKET transform.
+ *
+ * This is the drop-in boundary for the reference's hot path: the numba
+ * kernel call in gridrocket's engine
+ *
+ *     kernel(x[start:start+count], bank.lengths, bank.dilations, bank.paddings,
+ *            biases, wflat, bank.weight_offsets, bank.channel_indices,
+ *            bank.channel_offsets, bank.channel_counts,
+ *            limits.workers_per_cell, fpk, out, row0 + start) -> executed
+ *
+ * (/root/reference/pkg/src/gridrocket/engine.py:280-295, selecting
+ * _run_batch at engine.py:148-190).  Every entry point takes plain pointers
+ * and sizes; no torch or numpy types cross this boundary.  All functions
+ * return 0 on success and a nonzero RK_ERR_* code on failure; the message of
+ * the last failure on the calling thread is available from rk_last_error().
+ *
+ * Pointers named "x" and "out" may be host (pageable or pinned) or device
+ * memory; the library detects which with cudaPointerGetAttributes and moves
+ * data as needed.  Bank parameters are always host pointers.
+ */
+#ifndef ROCKET_B200_H
+#define ROCKET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_ABI_VERSION 1
+
+/* Error codes.  RK_ERR_CAPACITY mirrors gridrocket.CapacityError
+ * (engine.py:30-31); RK_ERR_INVALID mirrors the ValueError raised by
+ * _check_shapes / KernelBank.validate (engine.py:252-268, kernels.py:101-125). */
+#define RK_OK 0
+#define RK_ERR_INVALID 1
+#define RK_ERR_CAPACITY 2
+#define RK_ERR_CUDA 3
+#define RK_ERR_UNSUPPORTED 4
+#define RK_ERR_NO_DEVICE 5
+
+/* Arithmetic modes.
+ * RK_MODE_EXACT: every tap is RN(acc + RN(w*x)), channels ascending, taps
+ *   ascending, bias after the last tap — bit-identical to the reference's
+ *   single-precision engine (engine.py:172-180, reference.py:1-17).
+ * RK_MODE_FAST: fused multiply-add (FFMA2), bias folded into the
+ *   accumulator; within the north-star tolerance (MAX 1e-5 relative, PPV
+ *   exact except for outputs within 1e-6 of zero). */
+#define RK_MODE_EXACT 0
+#define RK_MODE_FAST 1
+
+typedef struct rk_bank_s* rk_bank_t;
+
+/* Summary of a device bank (the dilation-grouped layout). */
+typedef struct rk_bank_info_s {
+  int64_t n_kernels;
+  int32_t n_channels;
+  int32_t l_series;
+  int32_t n_groups;     /* distinct (length, dilation, padding, channel set) */
+  int32_t n_chunks;     /* warp work units (<= 4 kernels of one group) */
+  int32_t halo;         /* zero halo per side in the staged series (floats) */
+  int32_t smem_bytes;   /* dynamic shared memory per CTA */
+  int64_t positions_per_series; /* sum_k l_out_k == engine.total_positions */
+  int64_t useful_flops_per_series; /* sum_k 2*in-range taps + l_out_k */
+  int64_t device_bytes; /* device memory held by the bank */
+  int32_t device;
+  int32_t n_launches;   /* kernel launches per transform (non-empty classes) */
+} rk_bank_info_t;
+
+/* ABI version (RK_ABI_VERSION) and the thread-local last error message. */
+int rk_abi_version(void);
+const char* rk_last_error(void);
+
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int rk_device_count(int32_t* count);
+
+/* Build the device bank once per KernelBank.  The arrays are the columnar
+ * KernelBank fields (kernels.py:51-99) with weights and biases already cast
+ * to float32 as in engine._run_range (engine.py:275-276); weight_offsets and
+ * channel_offsets are KernelBank.weight_offsets / channel_offsets
+ * (kernels.py:84-88).  Replaces the per-batch argument list of the numba
+ * call at engine.py:280-295.  Fails with RK_ERR_CAPACITY when one staged
+ * series (all channels plus zero halos) does not fit in shared memory. */
+int rk_bank_create(int64_t n_kernels, int32_t n_channels, int32_t l_series,
+                   const int32_t* lengths, const int32_t* dilations,
+                   const int32_t* paddings, const float* biases,
+                   const float* weights, const int64_t* weight_offsets,
+                   const int32_t* channel_indices,
+                   const int64_t* channel_offsets,
+                   const int32_t* channel_counts, int32_t device,
+                   rk_bank_t* bank);
+int rk_bank_destroy(rk_bank_t bank);
+int rk_bank_info(rk_bank_t bank, rk_bank_info_t* info);
+
+/* Transform n_series series x[(n_series, n_channels, l_series) float32,
+ * C-contiguous] with every kernel of the bank and write rows
+ * [row0, row0 + n_series) of out (row stride ld_out floats) in the
+ * reference layout: out[row, k*fpk] = ppv_k, out[row, k*fpk + 1] = max_k
+ * (features.py:1-5, engine.py:186-188).  fpk is 2 (3 = MPV is not yet
+ * supported).  x and out may be host or device pointers.  stream is a
+ * cudaStream_t (NULL = the library's per-device stream); for device x and
+ * out the call is asynchronous on that stream, otherwise it returns after
+ * the features are in out.  *executed (may be NULL) receives the number of
+ * dot-product positions evaluated, counted on the device; it equals
+ * engine.expected_dot_products (engine.py:137-145). */
+int rk_transform_f32(rk_bank_t bank, const float* x, int64_t n_series,
+                     float* out, int64_t ld_out, int64_t row0, int32_t fpk,
+                     int32_t mode, void* stream, int64_t* executed);
+
+/* Stateless mirror of the numba entry point _run_batch
+ * (engine.py:148-190; called at engine.py:280-295): same arguments in the
+ * same order plus explicit sizes, returns the executed position count
+ * (>= 0) or -(RK_ERR_*) on failure.  The device bank is built on first use
+ * and cached by the identity and content of the bank arrays.  x and out are
+ * host pointers (the numpy arrays the engine passes); workers_per_cell is
+ * accepted for signature parity and, as in the reference, cannot change
+ * the result.  Uses RK_MODE_EXACT so results are byte-identical. */
+int64_t rk_run_batch_f32(const float* x, int64_t n_instances,
+                         int32_t n_channels, int32_t l_series,
+                         const int32_t* lengths, const int32_t* dilations,
+                         const int32_t* paddings, const float* biases,
+                         const float* wflat, const int64_t* woff,
+                         const int32_t* chidx, const int64_t* choff,
+                         const int32_t* chcnt, int64_t n_kernels,
+                         int32_t workers, int32_t fpk, float* out,
+                         int64_t ld_out, int64_t row0);
+
+/* Release cached banks and per-device buffers (optional at exit). */
+int rk_release_caches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROCKET_B200_H */

@@ -1,0 +1,690 @@
+// rocket_b200.cu — host runtime and C ABI of the B200 ROCKET transform.
+//
+//  * rk_bank_create builds the dilation-grouped device bank from the
+//    columnar KernelBank arrays (reference kernels.py:51-99);
+//  * rk_transform_f32 runs the transform over host or device series,
+//    pipelining H2D / kernel / D2H in row batches for host buffers;
+//  * rk_run_batch_f32 mirrors the reference's numba entry point
+//    engine._run_batch (engine.py:148-190, called at engine.py:280-295).
+#include "../../include/rocket_b200.h"
+#include "transform_kernel.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define RK_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(RK_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+constexpr int kLenIdx[12] = {-1, -1, -1, -1, -1, -1, -1, 0, -1, 1, -1, 2};
+
+struct HostChunk {
+  rk::DevChunk dev;
+  int64_t cost;  // instruction-slot estimate for one series
+};
+
+// Instruction-slot estimate of one chunk for one series at a given R
+// (positions per lane, stride = dilation).  Mirrors the kernel's lane map:
+// starts = A*d + min(d, rem), ceil(starts/32) warp steps.
+int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
+  const int64_t RD = (int64_t)R * d;
+  const int64_t A = n / RD;
+  const int64_t rem = n - A * RD;
+  const int64_t starts = A * d + std::min<int64_t>(d, rem);
+  const int64_t steps = (starts + 31) / 32;
+  const int64_t G = 2 * P;
+  const int64_t per_step = (int64_t)R * len * nc * P   // FFMA2
+                           + (int64_t)R * G * 3         // pooling epilogue
+                           + (int64_t)(R + len - 1) * nc  // window loads
+                           + 24;                        // lane map + loop
+  return steps * per_step + 40 * G;                     // + warp reduction / stores
+}
+
+}  // namespace
+
+struct rk_bank_s {
+  int device = 0;
+  int64_t K = 0;
+  int C = 0, L = 0;
+  int halo = 0;
+  int sstride = 0;
+  int smem_bytes = 0;
+  int n_groups = 0;
+  int64_t positions = 0;
+  int64_t useful_flops = 0;
+  std::vector<HostChunk> chunks;  // class-sorted
+  std::vector<int64_t> cost_prefix;
+  int cls_begin[rk::kNumClasses] = {};
+  int cls_end[rk::kNumClasses] = {};
+  rk::DevChunk* d_chunks = nullptr;
+  float* d_weights = nullptr;
+  int* d_chan_off = nullptr;
+  int64_t device_bytes = 0;
+  std::map<std::pair<int, int>, int*> d_block_start;  // (class, n_blocks) -> device boundaries
+  std::mutex mu;
+
+  ~rk_bank_s() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaFree(d_chunks);
+    cudaFree(d_weights);
+    cudaFree(d_chan_off);
+    for (auto& kv : d_block_start) cudaFree(kv.second);
+    cudaSetDevice(prev);
+  }
+
+  // Partition class cls's chunk range into nb blocks of near-equal cost.
+  int blocks_for(int cls, int nb, int** out) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(cls, nb);
+    auto it = d_block_start.find(key);
+    if (it != d_block_start.end()) {
+      *out = it->second;
+      return RK_OK;
+    }
+    const int cb = cls_begin[cls], ce = cls_end[cls];
+    std::vector<int> bs(nb + 1, cb);
+    const int64_t base = cost_prefix[cb], total = cost_prefix[ce] - base;
+    int ci = cb;
+    for (int b = 1; b < nb; ++b) {
+      const int64_t target = base + total * b / nb;
+      while (ci < ce && cost_prefix[ci + 1] <= target) ++ci;
+      bs[b] = std::max(ci, bs[b - 1]);
+    }
+    bs[nb] = ce;
+    int* d = nullptr;
+    RK_CUDA(cudaMalloc(&d, sizeof(int) * (nb + 1)));
+    RK_CUDA(cudaMemcpy(d, bs.data(), sizeof(int) * (nb + 1), cudaMemcpyHostToDevice));
+    d_block_start[key] = d;
+    *out = d;
+    return RK_OK;
+  }
+};
+
+namespace {
+
+struct DeviceState {
+  int sms = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::map<const void*, int> attr_smem;
+};
+std::mutex g_dev_mu;
+std::map<int, DeviceState> g_devs;
+
+int device_state(int device, DeviceState** out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_devs.find(device);
+  if (it == g_devs.end()) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return fail(RK_ERR_NO_DEVICE, "no CUDA device is visible");
+    }
+    if (device < 0 || device >= n) return fail(RK_ERR_INVALID, "device %d out of range [0, %d)", device, n);
+    DeviceState st;
+    RK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      return fail(RK_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
+                  prop.major, prop.minor);
+    st.sms = prop.multiProcessorCount;
+    st.smem_optin = prop.sharedMemPerBlockOptin;
+    RK_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+    RK_CUDA(cudaStreamCreateWithFlags(&st.copy_stream, cudaStreamNonBlocking));
+    it = g_devs.emplace(device, st).first;
+  }
+  *out = &it->second;
+  return RK_OK;
+}
+
+// Kernel table: one instantiation per (class, mode).
+using KernelFn = void (*)(const rk::LaunchArgs);
+template <int LEN, int R, int NCK>
+void fill_modes(KernelFn* t, int cls) {
+  t[2 * cls + 0] = rk::rocket_class_kernel<LEN, R, NCK, false>;
+  t[2 * cls + 1] = rk::rocket_class_kernel<LEN, R, NCK, true>;
+}
+template <int LEN, int R>
+void fill_nck(KernelFn* t, int li, int ri) {
+  const int base = (li * rk::kNumR + ri) * 3;
+  fill_modes<LEN, R, 0>(t, base + 0);
+  fill_modes<LEN, R, 1>(t, base + 1);
+  fill_modes<LEN, R, 2>(t, base + 2);
+}
+template <int LEN>
+void fill_r(KernelFn* t, int li) {
+  fill_nck<LEN, rk::r_of(0)>(t, li, 0);
+  fill_nck<LEN, rk::r_of(1)>(t, li, 1);
+  fill_nck<LEN, rk::r_of(2)>(t, li, 2);
+  fill_nck<LEN, rk::r_of(3)>(t, li, 3);
+}
+struct KernelTable {
+  KernelFn fn[2 * rk::kNumClasses];
+  KernelTable() {
+    fill_r<7>(fn, 0);
+    fill_r<9>(fn, 1);
+    fill_r<11>(fn, 2);
+  }
+};
+const KernelTable& kernel_table() {
+  static KernelTable t;
+  return t;
+}
+
+int set_kernel_smem(DeviceState* st, KernelFn fn, int bytes) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = st->attr_smem.find((const void*)fn);
+  if (it == st->attr_smem.end() || it->second < bytes) {
+    RK_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    st->attr_smem[(const void*)fn] = bytes;
+  }
+  return RK_OK;
+}
+
+bool is_device_pointer(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Enqueue the transform of n series already on the device: one launch per
+// non-empty chunk class, all on `stream`.
+int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
+           int mode, cudaStream_t stream, unsigned long long* d_exec) {
+  if (n <= 0) return RK_OK;
+  const int exact = mode == RK_MODE_EXACT ? 1 : 0;
+  const int series_bytes = b->smem_bytes;
+  const int smem_cap = (int)st->smem_optin - 1024;
+  for (int cls = 0; cls < rk::kNumClasses; ++cls) {
+    const int nchunks = b->cls_end[cls] - b->cls_begin[cls];
+    if (nchunks <= 0) continue;
+    KernelFn fn = kernel_table().fn[2 * cls + exact];
+    // Stage several series per item when the class is too small to keep
+    // all warps of a CTA busy on one series.
+    int spi = 1;
+    const int want = (4 * rk::kThreads / 32 + nchunks - 1) / nchunks;
+    while (spi < want && spi < 16 && (int64_t)(spi + 1) * series_bytes <= smem_cap / 2 && spi < n) ++spi;
+    const int smem = spi * series_bytes;
+    const int ctas_per_sm = 2 * smem + 2048 <= (int)st->smem_optin ? 2 : 1;
+    const int64_t resident = (int64_t)st->sms * ctas_per_sm;
+    const int64_t groups = (n + spi - 1) / spi;
+    int nb = 1;
+    while (nb < 64 && groups * nb < 4 * resident && nb * 2 <= nchunks / 8) nb *= 2;
+    int* d_bs = nullptr;
+    int rc = b->blocks_for(cls, nb, &d_bs);
+    if (rc) return rc;
+    rc = set_kernel_smem(st, fn, smem);
+    if (rc) return rc;
+    rk::LaunchArgs a;
+    a.x = d_x;
+    a.out = d_out;
+    a.ld_out = ld_out;
+    a.n_items = groups * nb;
+    a.n_series = n;
+    a.chunks = b->d_chunks;
+    a.weights = b->d_weights;
+    a.chan_off = b->d_chan_off;
+    a.block_start = d_bs;
+    a.executed = d_exec;
+    a.n_blocks = nb;
+    a.series_per_item = spi;
+    a.n_channels = b->C;
+    a.l_series = b->L;
+    a.halo = b->halo;
+    a.sstride = b->sstride;
+    a.fpk = fpk;
+    a.vec_out = (fpk == 2 && (ld_out % 2) == 0 && ((uintptr_t)d_out % 8) == 0) ? 1 : 0;
+    a.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
+    a.one = 1.0f;
+    const int64_t grid = std::min<int64_t>(a.n_items, resident);
+    fn<<<(unsigned)grid, rk::kThreads, smem, stream>>>(a);
+    RK_CUDA(cudaGetLastError());
+  }
+  return RK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rk_abi_version(void) { return RK_ABI_VERSION; }
+
+const char* rk_last_error(void) { return g_last_error.c_str(); }
+
+int rk_device_count(int32_t* count) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return RK_OK;
+}
+
+int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
+                   const int32_t* paddings, const float* biases, const float* weights,
+                   const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
+                   int32_t device, rk_bank_t* out) {
+  if (!out) return fail(RK_ERR_INVALID, "bank output pointer is NULL");
+  *out = nullptr;
+  if (K < 1) return fail(RK_ERR_INVALID, "bank must contain at least one kernel");
+  if (C < 1 || L < 1) return fail(RK_ERR_INVALID, "n_channels and l_series must be positive");
+  if (K > (int64_t)1 << 30) return fail(RK_ERR_CAPACITY, "%lld kernels exceed the device bank limit", (long long)K);
+  if (!lengths || !dilations || !paddings || !biases || !weights || !woff || !chidx || !choff || !chcnt)
+    return fail(RK_ERR_INVALID, "bank array pointer is NULL");
+
+  // ---- validate and key every kernel: (len, d, p, channel set) ----
+  struct Key {
+    int len, d, p;
+    std::vector<int> ch;
+    bool operator<(const Key& o) const { return std::tie(len, d, p, ch) < std::tie(o.len, o.d, o.p, o.ch); }
+  };
+  std::map<Key, std::vector<int64_t>> groups;
+  int halo = 0;
+  int64_t positions = 0, flops = 0;
+  for (int64_t k = 0; k < K; ++k) {
+    const int len = lengths[k], d = dilations[k], p = paddings[k], nc = chcnt[k];
+    if (len < 0 || len > 11 || kLenIdx[len] < 0)
+      return fail(RK_ERR_INVALID, "kernel %lld: length %d not in {7, 9, 11}", (long long)k, len);
+    if (d < 1) return fail(RK_ERR_INVALID, "kernel %lld: dilation %d must be >= 1", (long long)k, d);
+    if (p < 0) return fail(RK_ERR_INVALID, "kernel %lld: padding %d must be >= 0", (long long)k, p);
+    const int64_t l_out = (int64_t)L + 2 * (int64_t)p - (int64_t)(len - 1) * d;
+    if (l_out < 1)
+      return fail(RK_ERR_INVALID, "kernel %lld: span %lld exceeds padded series length %lld", (long long)k,
+                  (long long)(len - 1) * d, (long long)L + 2 * p);
+    if (nc < 1 || nc > C) return fail(RK_ERR_INVALID, "kernel %lld: channel count %d out of range", (long long)k, nc);
+    Key key{len, d, p, {}};
+    for (int s = 0; s < nc; ++s) {
+      const int ch = chidx[choff[k] + s];
+      if (ch < 0 || ch >= C) return fail(RK_ERR_INVALID, "kernel %lld: channel index %d out of range", (long long)k, ch);
+      key.ch.push_back(ch);
+    }
+    halo = std::max(halo, p);
+    positions += l_out;
+    // useful FLOPs: 2 per in-range tap + 1 bias add per output
+    int64_t taps = 0;
+    for (int j = 0; j < len; ++j) {
+      // positions t in [0, l_out) with 0 <= t - p + j*d < L
+      const int64_t off = (int64_t)j * d - p;
+      const int64_t t_lo = std::max<int64_t>(0, -off), t_hi = std::min<int64_t>(l_out, (int64_t)L - off);
+      if (t_hi > t_lo) taps += t_hi - t_lo;
+    }
+    flops += 2 * taps * nc + l_out;
+    groups[key].push_back(k);
+  }
+  if (halo > (1 << 24)) return fail(RK_ERR_CAPACITY, "padding %d too large", halo);
+
+  DeviceState* st = nullptr;
+  int rc = device_state(device, &st);
+  if (rc) return rc;
+
+  // Staged series: C channels of [halo zeros | L values | halo zeros],
+  // stride rounded to 32 floats + 1 bank offset between channels.
+  const int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + 4;
+  const int64_t smem = (int64_t)C * sstride * 4;
+  if (smem > (int64_t)st->smem_optin - 1024)
+    return fail(RK_ERR_CAPACITY,
+                "one staged series needs %lld bytes of shared memory (C=%d, L=%d, halo=%d) but a CTA has %zu",
+                (long long)smem, C, L, halo, st->smem_optin);
+
+  std::unique_ptr<rk_bank_s> b(new rk_bank_s());
+  b->device = device;
+  b->K = K;
+  b->C = C;
+  b->L = L;
+  b->halo = halo;
+  b->sstride = (int)sstride;
+  b->smem_bytes = (int)smem;
+  b->n_groups = (int)groups.size();
+  b->positions = positions;
+  b->useful_flops = flops;
+
+  std::vector<float> wpack;
+  std::vector<int> chan_off;
+  for (auto& kv : groups) {
+    const Key& key = kv.first;
+    const std::vector<int64_t>& ks = kv.second;
+    const int len = key.len, d = key.d, p = key.p, nc = (int)key.ch.size();
+    const int c = (len - 1) / 2;
+    const int n = L + 2 * p - (len - 1) * d;
+    const int nck = nc == 1 ? 0 : (nc == 2 ? 1 : 2);
+    const int P = nc == 1 ? 2 : 1;
+    const int G = 2 * P;
+    for (size_t k0 = 0; k0 < ks.size(); k0 += G) {
+      HostChunk hc;
+      std::memset(&hc.dev, 0, sizeof(hc.dev));
+      rk::DevChunk& dc = hc.dev;
+      const int nk = (int)std::min<size_t>(G, ks.size() - k0);
+      dc.len = len;
+      dc.d = d;
+      dc.lo = c * d - p;
+      dc.n = n;
+      dc.nk = nk;
+      dc.nc = nc;
+      // pick R (positions per lane) by the cost model
+      int best_r = 0;
+      int64_t best = INT64_MAX;
+      for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
+        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri));
+        if (cst < best) {
+          best = cst;
+          best_r = ri;
+        }
+      }
+      hc.cost = best;
+      dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * 3 + nck;
+      // weights: [slot][pair][tap][2], padded to 16 B
+      while (wpack.size() % 4) wpack.push_back(0.0f);
+      dc.wofs = (int)wpack.size();
+      for (int s = 0; s < nc; ++s)
+        for (int pp = 0; pp < P; ++pp)
+          for (int j = 0; j < len; ++j)
+            for (int h = 0; h < 2; ++h) {
+              const int g = 2 * pp + h;
+              float w = 0.0f;
+              if (g < nk) w = weights[woff[ks[k0 + g]] + (int64_t)s * len + j];
+              wpack.push_back(w);
+            }
+      dc.chofs = (int)chan_off.size();
+      for (int s = 0; s < nc; ++s) chan_off.push_back(key.ch[s] * (int)sstride);
+      for (int g = 0; g < 4; ++g) {
+        if (g < nk) {
+          const int64_t k = ks[k0 + g];
+          // -0.0 -> +0.0: identical results for the reference (acc is never -0),
+          // and keeps the fast path's accumulator init sign-clean.
+          const float bias = biases[k] + 0.0f;
+          dc.col[g] = (int)k;
+          dc.bias[g] = bias;
+        } else {
+          dc.col[g] = -1;
+          dc.bias[g] = 0.0f;
+        }
+      }
+      b->chunks.push_back(hc);
+    }
+  }
+  // thresholds depend on the mode only through the sign convention; the
+  // exact kernel compares acc > -bias, the fast kernel acc(+bias) > 0.
+  // Both are stored: thr holds -bias and the fast kernel ignores it.
+  for (auto& hc : b->chunks)
+    for (int g = 0; g < 4; ++g) hc.dev.thr[g] = -hc.dev.bias[g];
+  // class-major order (keeps the warps of a CTA in one code path), then
+  // descending cost (long chunks first, short ones fill the tail).
+  std::stable_sort(b->chunks.begin(), b->chunks.end(), [](const HostChunk& x, const HostChunk& y) {
+    if (x.dev.cls != y.dev.cls) return x.dev.cls < y.dev.cls;
+    return x.cost > y.cost;
+  });
+  for (int c = 0; c < rk::kNumClasses; ++c) b->cls_begin[c] = b->cls_end[c] = 0;
+  for (size_t i = 0; i < b->chunks.size(); ++i) {
+    const int c = b->chunks[i].dev.cls;
+    if (i == 0 || b->chunks[i - 1].dev.cls != c) b->cls_begin[c] = (int)i;
+    b->cls_end[c] = (int)i + 1;
+  }
+  b->cost_prefix.assign(b->chunks.size() + 1, 0);
+  for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
+
+  std::vector<rk::DevChunk> dev(b->chunks.size());
+  for (size_t i = 0; i < b->chunks.size(); ++i) dev[i] = b->chunks[i].dev;
+  if (wpack.empty()) wpack.push_back(0.0f);
+  RK_CUDA(cudaSetDevice(device));
+  RK_CUDA(cudaMalloc(&b->d_chunks, sizeof(rk::DevChunk) * dev.size()));
+  RK_CUDA(cudaMalloc(&b->d_weights, sizeof(float) * wpack.size()));
+  RK_CUDA(cudaMalloc(&b->d_chan_off, sizeof(int) * chan_off.size()));
+  RK_CUDA(cudaMemcpy(b->d_chunks, dev.data(), sizeof(rk::DevChunk) * dev.size(), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(b->d_weights, wpack.data(), sizeof(float) * wpack.size(), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(b->d_chan_off, chan_off.data(), sizeof(int) * chan_off.size(), cudaMemcpyHostToDevice));
+  b->device_bytes = (int64_t)(sizeof(rk::DevChunk) * dev.size() + sizeof(float) * wpack.size() +
+                              sizeof(int) * chan_off.size());
+  *out = b.release();
+  return RK_OK;
+}
+
+int rk_bank_destroy(rk_bank_t bank) {
+  delete bank;
+  return RK_OK;
+}
+
+int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
+  if (!b || !info) return fail(RK_ERR_INVALID, "NULL bank or info");
+  std::memset(info, 0, sizeof(*info));
+  info->n_kernels = b->K;
+  info->n_channels = b->C;
+  info->l_series = b->L;
+  info->n_groups = b->n_groups;
+  info->n_chunks = (int32_t)b->chunks.size();
+  info->halo = b->halo;
+  info->smem_bytes = b->smem_bytes;
+  info->positions_per_series = b->positions;
+  info->useful_flops_per_series = b->useful_flops;
+  info->device_bytes = b->device_bytes;
+  info->device = b->device;
+  for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;
+  return RK_OK;
+}
+
+int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t ld_out, int64_t row0,
+                     int32_t fpk, int32_t mode, void* stream_ptr, int64_t* executed) {
+  if (!b) return fail(RK_ERR_INVALID, "NULL bank");
+  if (n < 0 || row0 < 0) return fail(RK_ERR_INVALID, "n_series and row0 must be non-negative");
+  if (fpk != 2) return fail(RK_ERR_UNSUPPORTED, "features_per_kernel=%d: only 2 (ppv, max) is implemented", fpk);
+  if (mode != RK_MODE_EXACT && mode != RK_MODE_FAST) return fail(RK_ERR_INVALID, "unknown mode %d", mode);
+  if (ld_out < b->K * fpk) return fail(RK_ERR_INVALID, "ld_out %lld < n_kernels * fpk", (long long)ld_out);
+  if (executed) *executed = 0;
+  if (n == 0) return RK_OK;
+  if (!x || !out) return fail(RK_ERR_INVALID, "NULL x or out");
+  DeviceState* st = nullptr;
+  int rc = device_state(b->device, &st);
+  if (rc) return rc;
+  RK_CUDA(cudaSetDevice(b->device));
+  const bool dx = is_device_pointer(x), dout = is_device_pointer(out);
+  const int64_t row_in = (int64_t)b->C * b->L;
+  if (dx && dout) {
+    // Device-resident: asynchronous on the caller's stream (or the
+    // library's); the executed counter is private to this call.
+    cudaStream_t stream = stream_ptr ? (cudaStream_t)stream_ptr : st->stream;
+    unsigned long long* d_exec = nullptr;
+    RK_CUDA(cudaMallocAsync(&d_exec, sizeof(unsigned long long), stream));
+    RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
+    rc = launch(b, st, x, n, out + row0 * ld_out, ld_out, fpk, mode, stream, d_exec);
+    if (rc) return rc;
+    if (executed) {
+      unsigned long long h = 0;
+      RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));
+      RK_CUDA(cudaFreeAsync(d_exec, stream));
+      RK_CUDA(cudaStreamSynchronize(stream));
+      *executed = (int64_t)h;
+    } else {
+      RK_CUDA(cudaFreeAsync(d_exec, stream));
+    }
+    return RK_OK;
+  }
+  // Host buffers: row batches through device scratch on two private
+  // streams (reentrant per call), double-buffered so batch i+1's H2D and
+  // batch i-1's D2H overlap batch i's kernels.
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  RK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  RK_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  const int64_t out_row_bytes = b->K * fpk * 4;
+  const int64_t in_row_bytes = row_in * 4;
+  const int64_t budget = (int64_t)1 << 30;  // device scratch per buffer
+  int64_t batch = std::max<int64_t>(1, budget / (out_row_bytes + in_row_bytes));
+  batch = std::min<int64_t>(batch, n);
+  // at least two batches in flight when there is enough work to overlap
+  if (n >= 4096) batch = std::min<int64_t>(batch, (n + 3) / 4);
+  float* d_in[2] = {nullptr, nullptr};
+  float* d_o[2] = {nullptr, nullptr};
+  unsigned long long* d_exec = nullptr;
+  cudaEvent_t ev_done[2];
+  RK_CUDA(cudaMallocAsync(&d_exec, sizeof(unsigned long long), stream));
+  for (int i = 0; i < 2; ++i) {
+    if (!dx) RK_CUDA(cudaMallocAsync(&d_in[i], batch * in_row_bytes, stream));
+    if (!dout) RK_CUDA(cudaMallocAsync(&d_o[i], batch * out_row_bytes, stream));
+    RK_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  }
+  RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
+  int64_t bi = 0;
+  for (int64_t s0 = 0; s0 < n; s0 += batch, ++bi) {
+    const int64_t cnt = std::min(batch, n - s0);
+    const int k = (int)(bi & 1);
+    const float* kx = x + s0 * row_in;
+    if (!dx) {
+      RK_CUDA(cudaMemcpyAsync(d_in[k], kx, cnt * in_row_bytes, cudaMemcpyHostToDevice, stream));
+      kx = d_in[k];
+    }
+    float* ko = dout ? out + (row0 + s0) * ld_out : d_o[k];
+    const int64_t kld = dout ? ld_out : b->K * fpk;
+    rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec);
+    if (rc) return rc;
+    if (!dout) {
+      // D2H on the copy stream so the next batch's kernels can start.
+      RK_CUDA(cudaEventRecord(ev_done[k], stream));
+      RK_CUDA(cudaStreamWaitEvent(copy_stream, ev_done[k], 0));
+      float* hdst = out + (row0 + s0) * ld_out;
+      if (ld_out == kld) {
+        RK_CUDA(cudaMemcpyAsync(hdst, d_o[k], cnt * out_row_bytes, cudaMemcpyDeviceToHost, copy_stream));
+      } else {
+        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, d_o[k], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
+                                  copy_stream));
+      }
+      // the next use of buffer k waits for this copy
+      RK_CUDA(cudaEventRecord(ev_done[k], copy_stream));
+      RK_CUDA(cudaStreamWaitEvent(stream, ev_done[k], 0));
+    }
+  }
+  unsigned long long h = 0;
+  RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  RK_CUDA(cudaStreamSynchronize(copy_stream));
+  for (int i = 0; i < 2; ++i) {
+    if (d_in[i]) RK_CUDA(cudaFreeAsync(d_in[i], stream));
+    if (d_o[i]) RK_CUDA(cudaFreeAsync(d_o[i], stream));
+  }
+  RK_CUDA(cudaFreeAsync(d_exec, stream));
+  RK_CUDA(cudaStreamSynchronize(stream));
+  for (int i = 0; i < 2; ++i) cudaEventDestroy(ev_done[i]);
+  cudaStreamDestroy(stream);
+  cudaStreamDestroy(copy_stream);
+  if (executed) *executed = (int64_t)h;
+  return RK_OK;
+}
+
+// ---- stateless drop-in for engine._run_batch ----------------------------
+namespace {
+struct CacheKey {
+  const void* p[10];
+  int64_t K;
+  int C, L;
+  uint64_t hash;
+  bool operator<(const CacheKey& o) const {
+    return std::memcmp(this, &o, sizeof(CacheKey)) < 0;
+  }
+};
+std::mutex g_cache_mu;
+std::map<CacheKey, rk_bank_t> g_cache;
+
+uint64_t fnv(uint64_t h, const void* data, size_t bytes) {
+  const unsigned char* c = (const unsigned char*)data;
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= c[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+}  // namespace
+
+int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                         const int32_t* dilations, const int32_t* paddings, const float* biases,
+                         const float* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
+                         const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, float* out,
+                         int64_t ld_out, int64_t row0) {
+  if (workers < 1) return -fail(RK_ERR_INVALID, "workers_per_cell must be positive");
+  if (K < 1) return -fail(RK_ERR_INVALID, "bank must contain at least one kernel");
+  int64_t nw = 0, nci = 0;
+  for (int64_t k = 0; k < K; ++k) {
+    nw = std::max<int64_t>(nw, woff[k] + (int64_t)lengths[k] * chcnt[k]);
+    nci = std::max<int64_t>(nci, choff[k] + chcnt[k]);
+  }
+  CacheKey key;
+  std::memset(&key, 0, sizeof(key));
+  const void* ptrs[10] = {lengths, dilations, paddings, biases, wflat, woff, chidx, choff, chcnt, nullptr};
+  for (int i = 0; i < 10; ++i) key.p[i] = ptrs[i];
+  key.K = K;
+  key.C = C;
+  key.L = L;
+  uint64_t h = 1469598103934665603ull;
+  h = fnv(h, lengths, 4 * K);
+  h = fnv(h, dilations, 4 * K);
+  h = fnv(h, paddings, 4 * K);
+  h = fnv(h, biases, 4 * K);
+  h = fnv(h, chcnt, 4 * K);
+  h = fnv(h, wflat, 4 * nw);
+  h = fnv(h, chidx, 4 * nci);
+  key.hash = h;
+  rk_bank_t bank = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) bank = it->second;
+  }
+  if (!bank) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int rc = rk_bank_create(K, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx, choff, chcnt, dev,
+                            &bank);
+    if (rc) return -rc;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (g_cache.size() >= 8) {
+      rk_bank_destroy(g_cache.begin()->second);
+      g_cache.erase(g_cache.begin());
+    }
+    g_cache[key] = bank;
+  }
+  int64_t executed = 0;
+  int rc = rk_transform_f32(bank, x, n_inst, out, ld_out, row0, fpk, RK_MODE_EXACT, nullptr, &executed);
+  if (rc) return -rc;
+  return executed;
+}
+
+int rk_release_caches(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& kv : g_cache) rk_bank_destroy(kv.second);
+  g_cache.clear();
+  return RK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""Generate the golden fixtures from the reference implementation.
+
+Run HERE (the container that mounts /root/reference); the outputs are
+committed under tests/golden/ so the GPU box, which has no /root/reference,
+can check parity:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Fixtures:
+  banks.json      fingerprints of reference banks (gridrocket.generate_bank,
+                  kernels.py:243-308) for every bank the tests use;
+  transforms.npz  reference features (gridrocket.transform, engine.py:324-333,
+                  precision single/double, with and without MPV) for seeded
+                  inputs; inputs are regenerated from their seeds by
+                  tests/golden_cases.py, which defines the cases.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(REPO, "tests"))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+
+import gridrocket as gr  # noqa: E402
+
+import golden_cases as gc  # noqa: E402
+
+
+def fingerprint(bank):
+    import hashlib
+
+    h = hashlib.sha256()
+    for arr in (bank.lengths, bank.weights, bank.biases, bank.dilations, bank.paddings,
+                bank.channel_counts, bank.channel_indices):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()[:16]
+
+
+def survey_fingerprint(bank):
+    import hashlib
+
+    h = hashlib.sha256()
+    for arr in (bank.lengths, bank.weights, bank.biases, bank.dilations, bank.paddings):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()[:16]
+
+
+def ref_bank(spec):
+    if spec[0] == "gen":
+        _, l, c, k, seed = spec
+        return gr.generate_bank(l, c, k, gr.GenOptions(seed=seed))
+    fields = gc.custom_bank_fields(spec)
+    return gr.KernelBank(**fields)
+
+
+def main():
+    banks = {}
+    for name, spec in gc.BANKS.items():
+        b = ref_bank(spec)
+        banks[name] = {
+            "spec": list(spec),
+            "fingerprint": fingerprint(b),
+            "survey_fingerprint": survey_fingerprint(b),
+            "count": int(b.count),
+            "lengths_head": b.lengths[:8].tolist(),
+            "dilations_head": b.dilations[:8].tolist(),
+            "paddings_head": b.paddings[:8].tolist(),
+            "biases_head": b.biases[:4].tolist(),
+            "total_positions": int(gr.engine.total_positions(b)),
+        }
+        print(name, banks[name]["fingerprint"], flush=True)
+    with open(os.path.join(HERE, "banks.json"), "w") as f:
+        json.dump({"numpy": np.__version__, "banks": banks}, f, indent=1)
+
+    arrays = {}
+    for name, case in gc.CASES.items():
+        values = gc.case_values(case)
+        bank = ref_bank(gc.BANKS[case["bank"]])
+        for variant in case["variants"]:
+            mpv = variant.endswith("_mpv")
+            precision = variant.split("_")[0]
+            fm, stats = gr.transform_with_stats(values, bank, include_mpv=mpv, precision=precision)
+            arrays[f"{name}/{variant}"] = fm.values
+            arrays[f"{name}/{variant}/executed"] = np.array([stats.total_dot_products], dtype=np.int64)
+        print(name, values.shape, flush=True)
+    np.savez_compressed(os.path.join(HERE, "transforms.npz"), **arrays)
+
+
+if __name__ == "__main__":
+    main()

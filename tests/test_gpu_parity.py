@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA transform (through the C ABI) vs the reference.
+
+Exact mode must be byte-identical to the reference's single-precision
+engine (golden fixtures from gridrocket.transform, and the pinned oracle);
+fast mode must meet the north-star tolerance (tests/parity.py)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+from parity import check_fast
+from paper_2601_17091_b200 import (
+    CapacityError,
+    GenOptions,
+    GridLimits,
+    device_bank,
+    expected_dot_products,
+    generate_bank,
+    synth_random,
+    transform,
+    transform_sharded,
+    transform_with_stats,
+)
+
+pytestmark = pytest.mark.gpu
+SINGLE = [name for name, case in gc.CASES.items() if "single" in case["variants"]]
+
+
+def _case(name):
+    case = gc.CASES[name]
+    return gc.case_values(case), gc.make_bank(gc.BANKS[case["bank"]])
+
+
+@pytest.mark.parametrize("name", SINGLE)
+def test_exact_bytes_match_reference(name, golden_transforms, cuda_ready):
+    values, bank = _case(name)
+    fm, stats = transform_with_stats(values, bank, mode="exact")
+    ref = golden_transforms[f"{name}/single"]
+    assert fm.values.dtype == np.float32 and fm.values.shape == ref.shape
+    assert fm.values.tobytes() == ref.tobytes()
+    assert stats.total_dot_products == int(golden_transforms[f"{name}/single/executed"][0])
+
+
+@pytest.mark.parametrize("name", SINGLE)
+def test_fast_within_tolerance(name, golden_transforms, cuda_ready):
+    values, bank = _case(name)
+    fm = transform(values, bank, mode="fast")
+    check_fast(fm.values, golden_transforms[f"{name}/single"], values, bank)
+
+
+def test_run_batch_dropin_signature(golden_transforms, cuda_ready):
+    """rk_run_batch_f32 takes _run_batch's argument list (engine.py:148-150)."""
+    lib = cuda_ready
+    values, bank = _case("rc7")
+    x = np.ascontiguousarray(values, dtype=np.float32)
+    out = np.full((x.shape[0] + 3, bank.count * 2), np.nan, dtype=np.float32)
+    a = dict(
+        lengths=bank.lengths, dilations=bank.dilations, paddings=bank.paddings,
+        biases=bank.biases.astype(np.float32), wflat=bank.weights.astype(np.float32),
+        woff=bank.weight_offsets, chidx=bank.channel_indices, choff=bank.channel_offsets,
+        chcnt=bank.channel_counts,
+    )
+    a = {k: np.ascontiguousarray(v) for k, v in a.items()}
+    p = lambda arr: arr.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    executed = lib.rk_run_batch_f32(
+        p(x), x.shape[0], x.shape[1], x.shape[2], p(a["lengths"]), p(a["dilations"]), p(a["paddings"]),
+        p(a["biases"]), p(a["wflat"]), p(a["woff"]), p(a["chidx"]), p(a["choff"]), p(a["chcnt"]),
+        bank.count, 1024, 2, p(out), out.shape[1], 3,
+    )
+    assert executed == expected_dot_products(bank, x.shape[0])
+    assert np.isnan(out[:3]).all()
+    assert out[3:].tobytes() == golden_transforms["rc7/single"].tobytes()
+
+
+def test_sharding_and_batching_are_pure_partitions(cuda_ready):
+    values, bank = _case("rc300")
+    whole = transform(values, bank)
+    assert transform_sharded(values, bank, 4).values.tobytes() == whole.values.tobytes()
+    fm, stats = transform_with_stats(values, bank, limits=GridLimits(max_y=7, workers_per_cell=3))
+    assert fm.values.tobytes() == whole.values.tobytes()
+    assert stats.n_batches == -(-values.shape[0] // 7)
+    assert stats.total_dot_products == expected_dot_products(bank, values.shape[0])
+    empty = transform_sharded(np.zeros((0, 1, bank.l_series)), bank, 3)
+    assert empty.values.shape == (0, bank.count * 2)
+
+
+def test_fast_mode_is_deterministic(cuda_ready):
+    values, bank = _case("l1024")
+    a = transform(values, bank, mode="fast").values
+    b = transform(values, bank, mode="fast").values
+    assert a.tobytes() == b.tobytes()
+
+
+def test_device_pointer_path_matches_host_path(golden_transforms, cuda_ready):
+    import torch
+
+    values, bank = _case("mv2048")
+    db = device_bank(bank, 0)
+    x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).cuda()
+    out = torch.full((x.shape[0] + 1, bank.count * 2), float("nan"), device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    executed = db.transform_into(x.data_ptr(), x.shape[0], out.data_ptr(), out.shape[1], row0=1,
+                                 mode="exact", stream=stream)
+    torch.cuda.synchronize()
+    assert executed == expected_dot_products(bank, x.shape[0])
+    got = out.cpu().numpy()
+    assert np.isnan(got[0]).all()
+    assert got[1:].tobytes() == golden_transforms["mv2048/single"].tobytes()
+
+
+def test_config2_rows_exact_vs_oracle(cuda_ready):
+    """BASELINE config 2 shape (L=1024, 10k kernels) on a 192-series slice."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(1024, 1, 10000, GenOptions(seed=0))
+    values = synth_random(192, 1, 1024, seed=1).values
+    got = transform(values, bank, mode="exact").values
+    assert got.tobytes() == oracle_transform(values, bank).tobytes()
+
+
+def test_config5_multichannel_exact_vs_oracle(cuda_ready):
+    """BASELINE config 5 shape (3 channels, L=2048) at 10k kernels, 24 series."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(2048, 3, 10000, GenOptions(seed=0))
+    values = synth_random(24, 3, 2048, seed=1).values
+    got = transform(values, bank, mode="exact").values
+    assert got.tobytes() == oracle_transform(values, bank).tobytes()
+    fast = transform(values, bank, mode="fast").values
+    check_fast(fast, got, values, bank)
+
+
+def test_full_size_config2_properties(cuda_ready):
+    """Full BASELINE config 2 (100k x 1024, 10k kernels) device-resident:
+    size-independent properties + sampled rows vs the oracle."""
+    import torch
+
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(1024, 1, 10000, GenOptions(seed=0))
+    n = 100_000
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn((n, 1, 1024), device="cuda", generator=g, dtype=torch.float32)
+    out = torch.empty((n, bank.count * 2), device="cuda", dtype=torch.float32)
+    db = device_bank(bank, 0)
+    executed = db.transform_into(x.data_ptr(), n, out.data_ptr(), out.shape[1], mode="exact",
+                                 stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert executed == expected_dot_products(bank, n)
+    ppv = out[:, 0::2]
+    l_out = torch.from_numpy(bank.output_lengths()).cuda().to(torch.float64)
+    counts = ppv.to(torch.float64) * l_out
+    assert torch.all((counts - counts.round()).abs() < 1e-3)
+    assert torch.all((ppv >= 0) & (ppv <= 1))
+    rows = torch.tensor([0, 1, 4242, 50_000, 77_777, n - 1], device="cuda")
+    sample = x[rows].cpu().numpy()
+    assert out[rows].cpu().numpy().tobytes() == oracle_transform(sample, bank).tobytes()
+
+
+def test_errors_mirror_reference(cuda_ready):
+    values, bank = _case("small")
+    with pytest.raises(ValueError):
+        transform(np.zeros((2, 2, 64)), bank)
+    with pytest.raises(ValueError):
+        transform(np.zeros((2, 1, 32)), bank)
+    bad = np.zeros((2, 1, 64))
+    bad[1, 0, 5] = np.inf
+    with pytest.raises(ValueError):
+        transform(bad, bank)
+    with pytest.raises(CapacityError):
+        transform(values, bank, limits=GridLimits(max_x=3))
+    with pytest.raises(ValueError):
+        transform(values, bank, mode="approximate")
+    big = generate_bank(200_000, 1, 4, GenOptions(seed=3))
+    with pytest.raises(CapacityError):
+        transform(np.zeros((1, 1, 200_000), dtype=np.float32), big)
