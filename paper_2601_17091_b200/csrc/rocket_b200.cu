@@ -53,22 +53,26 @@ struct HostChunk {
 };
 
 // Instruction-slot estimate of one chunk for one series at a given R
-// (positions per lane, stride = dilation).  Mirrors the kernel's lane map:
-// starts = A*d + min(d, rem), ceil(starts/32) warp steps.
+// (positions per lane, stride = dilation), following the kernel's lane map
+// (run_positions): full 32-lane steps of R positions, then 1-position
+// masked steps for the leftover positions.
 int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
+  const int64_t G = 2 * P;
   const int64_t RD = (int64_t)R * d;
   const int64_t A = n / RD;
-  const int64_t rem = n - A * RD;
-  const int64_t starts = A * d + std::min<int64_t>(d, rem);
-  const int64_t steps = (starts + 31) / 32;
-  const int64_t G = 2 * P;
-  const int64_t per_step = (int64_t)R * len * nc * P   // FFMA2
-                           + (int64_t)R * G * 3         // pooling epilogue
-                           + (int64_t)(R + len - 1) * nc  // window loads
-                           + 24;                        // lane map + loop
-  return steps * per_step + 40 * G;                     // + warp reduction / stores
+  const int64_t full_starts = A * d;
+  const int64_t nfull = full_starts / 32;
+  const int64_t left = (full_starts - nfull * 32) * R + (n - A * RD);
+  const int64_t tail_steps = (left + 31) / 32;
+  auto step = [&](int64_t r, int64_t extra) {
+    return r * len * nc * P              // FFMA2
+           + r * G * 2                   // count (FSETP + IADD)
+           + (r * G + 1) / 2             // max (FMNMX3 pairs)
+           + 2 * (r + len - 1) * nc      // window loads + addresses
+           + extra;
+  };
+  return nfull * step(R, 8) + tail_steps * step(1, 30) + 40 * G + 60;
 }
-
 }  // namespace
 
 struct rk_bank_s {
@@ -179,10 +183,11 @@ void fill_modes(KernelFn* t, int cls) {
 }
 template <int LEN, int R>
 void fill_nck(KernelFn* t, int li, int ri) {
-  const int base = (li * rk::kNumR + ri) * 3;
+  const int base = (li * rk::kNumR + ri) * rk::kNumNck;
   fill_modes<LEN, R, 0>(t, base + 0);
   fill_modes<LEN, R, 1>(t, base + 1);
-  fill_modes<LEN, R, 2>(t, base + 2);
+  fill_modes<LEN, R, 3>(t, base + 3);
+  if constexpr (R == 1) fill_modes<LEN, R, 2>(t, base + 2);  // generic path: 1 position per lane
 }
 template <int LEN>
 void fill_r(KernelFn* t, int li) {
@@ -192,7 +197,7 @@ void fill_r(KernelFn* t, int li) {
   fill_nck<LEN, rk::r_of(3)>(t, li, 3);
 }
 struct KernelTable {
-  KernelFn fn[2 * rk::kNumClasses];
+  KernelFn fn[2 * rk::kNumClasses] = {};
   KernelTable() {
     fill_r<7>(fn, 0);
     fill_r<9>(fn, 1);
@@ -309,11 +314,16 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   if (!lengths || !dilations || !paddings || !biases || !weights || !woff || !chidx || !choff || !chcnt)
     return fail(RK_ERR_INVALID, "bank array pointer is NULL");
 
-  // ---- validate and key every kernel: (len, d, p, channel set) ----
+  // ---- validate and key every kernel ----
+  // Group key (dilation, lo, n, channel set): all kernels of a group share
+  // the centre-position range [lo, lo + n) (lo = c*d - p, n = l_out), so
+  // centred-padded kernels of every length share one group; shorter
+  // kernels sit zero-padded inside a longer chunk (exact: zero taps add
+  // +-0, which never changes the reference sum).
   struct Key {
-    int len, d, p;
+    int d, lo, n;
     std::vector<int> ch;
-    bool operator<(const Key& o) const { return std::tie(len, d, p, ch) < std::tie(o.len, o.d, o.p, o.ch); }
+    bool operator<(const Key& o) const { return std::tie(d, lo, n, ch) < std::tie(o.d, o.lo, o.n, o.ch); }
   };
   std::map<Key, std::vector<int64_t>> groups;
   int halo = 0;
@@ -328,8 +338,10 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     if (l_out < 1)
       return fail(RK_ERR_INVALID, "kernel %lld: span %lld exceeds padded series length %lld", (long long)k,
                   (long long)(len - 1) * d, (long long)L + 2 * p);
+    if ((int64_t)(len - 1) / 2 * d + L + p > (int64_t)1 << 30)
+      return fail(RK_ERR_CAPACITY, "kernel %lld: dilation/padding too large", (long long)k);
     if (nc < 1 || nc > C) return fail(RK_ERR_INVALID, "kernel %lld: channel count %d out of range", (long long)k, nc);
-    Key key{len, d, p, {}};
+    Key key{d, (len - 1) / 2 * d - p, (int)l_out, {}};
     for (int s = 0; s < nc; ++s) {
       const int ch = chidx[choff[k] + s];
       if (ch < 0 || ch >= C) return fail(RK_ERR_INVALID, "kernel %lld: channel index %d out of range", (long long)k, ch);
@@ -379,28 +391,42 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   std::vector<int> chan_off;
   for (auto& kv : groups) {
     const Key& key = kv.first;
-    const std::vector<int64_t>& ks = kv.second;
-    const int len = key.len, d = key.d, p = key.p, nc = (int)key.ch.size();
-    const int c = (len - 1) / 2;
-    const int n = L + 2 * p - (len - 1) * d;
-    const int nck = nc == 1 ? 0 : (nc == 2 ? 1 : 2);
-    const int P = nc == 1 ? 2 : 1;
-    const int G = 2 * P;
-    for (size_t k0 = 0; k0 < ks.size(); k0 += G) {
+    std::vector<int64_t> ks = kv.second;
+    // longest kernels first: chunks are length-homogeneous except at the
+    // boundaries between lengths
+    std::stable_sort(ks.begin(), ks.end(), [&](int64_t x, int64_t y) { return lengths[x] > lengths[y]; });
+    const int d = key.d, nc = (int)key.ch.size();
+    const int n = key.n;
+    size_t k0 = 0;
+    while (k0 < ks.size()) {
+      const size_t left = ks.size() - k0;
+      // 1-channel groups: 4-kernel chunks (2 FFMA2 pairs), 1-pair chunks
+      // for a remainder of 1 or 2; multichannel: 1 pair per chunk.
+      int P, nck;
+      if (nc == 1) {
+        P = left >= 3 ? 2 : 1;
+        nck = P == 2 ? 0 : 3;
+      } else {
+        P = 1;
+        nck = nc == 2 ? 1 : 2;
+      }
+      const int G = 2 * P;
+      const int nk = (int)std::min<size_t>(G, left);
+      const int len = lengths[ks[k0]];
+      const int cc = (len - 1) / 2;
       HostChunk hc;
       std::memset(&hc.dev, 0, sizeof(hc.dev));
       rk::DevChunk& dc = hc.dev;
-      const int nk = (int)std::min<size_t>(G, ks.size() - k0);
       dc.len = len;
       dc.d = d;
-      dc.lo = c * d - p;
+      dc.lo = key.lo;
       dc.n = n;
       dc.nk = nk;
       dc.nc = nc;
-      // pick R (positions per lane) by the cost model
       int best_r = 0;
       int64_t best = INT64_MAX;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
+        if (nck == 2 && ri != 0) continue;  // generic path is 1 position per lane
         const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri));
         if (cst < best) {
           best = cst;
@@ -408,8 +434,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         }
       }
       hc.cost = best;
-      dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * 3 + nck;
-      // weights: [slot][pair][tap][2], padded to 16 B
+      dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
+      // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is
+      // centred in the LEN-tap frame with zero taps at both ends.
       while (wpack.size() % 4) wpack.push_back(0.0f);
       dc.wofs = (int)wpack.size();
       for (int s = 0; s < nc; ++s)
@@ -418,7 +445,12 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
             for (int h = 0; h < 2; ++h) {
               const int g = 2 * pp + h;
               float w = 0.0f;
-              if (g < nk) w = weights[woff[ks[k0 + g]] + (int64_t)s * len + j];
+              if (g < nk) {
+                const int64_t k = ks[k0 + g];
+                const int lk = lengths[k], ck = (lk - 1) / 2;
+                const int jj = j - (cc - ck);
+                if (jj >= 0 && jj < lk) w = weights[woff[k] + (int64_t)s * lk + jj];
+              }
               wpack.push_back(w);
             }
       dc.chofs = (int)chan_off.size();
@@ -437,13 +469,16 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         }
       }
       b->chunks.push_back(hc);
+      k0 += nk;
     }
   }
   // thresholds depend on the mode only through the sign convention; the
   // exact kernel compares acc > -bias, the fast kernel acc(+bias) > 0.
   // Both are stored: thr holds -bias and the fast kernel ignores it.
+  // exact: count acc > -bias (RN(acc + b) > 0 <=> acc > -b); "+ 0.0f"
+  // keeps the threshold off -0 (the kernel's compare is a plain setp.gt).
   for (auto& hc : b->chunks)
-    for (int g = 0; g < 4; ++g) hc.dev.thr[g] = -hc.dev.bias[g];
+    for (int g = 0; g < 4; ++g) hc.dev.thr[g] = -hc.dev.bias[g] + 0.0f;
   // class-major order (keeps the warps of a CTA in one code path), then
   // descending cost (long chunks first, short ones fill the tail).
   std::stable_sort(b->chunks.begin(), b->chunks.end(), [](const HostChunk& x, const HostChunk& y) {

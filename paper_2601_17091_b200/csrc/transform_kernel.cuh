@@ -27,10 +27,13 @@ constexpr int kMinBlocks = 2;      // 2 CTAs / SM  -> <= 128 registers
 constexpr int kChunkKernels = 4;   // kernels per chunk (2 FFMA2 pairs)
 constexpr unsigned kFull = 0xffffffffu;
 
-// Class encoding: cls = ((len_idx * kNumR) + r_idx) * 3 + nc_kind
+// Class encoding: cls = ((len_idx * kNumR) + r_idx) * kNumNck + nc_kind
+//   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
+//           2: >= 3 channels (generic); 3: 1 channel, 1 pair
 constexpr int kNumR = 4;
 __host__ __device__ constexpr int r_of(int r_idx) { return 2 * r_idx + 1; }  // 1,3,5,7
-constexpr int kNumClasses = 3 * kNumR * 3;
+constexpr int kNumNck = 4;
+constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
 // One warp work unit.  All kernels of a chunk have the same length,
 // dilation, padding and channel set, hence the same valid centre-position
@@ -112,16 +115,13 @@ __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w
   }
 }
 
-template <int LEN, int R, bool MASKED>
-__device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
-                                            int u0, int d, int lo_clamp, int hi_clamp) {
+template <int LEN, int R>
+__device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const float* __restrict__ chan, int u0,
+                                            int d) {
   constexpr int C = (LEN - 1) / 2;
+  const float* p = chan + (u0 - C * d);
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) {
-    int idx = u0 + (q - C) * d;
-    if (MASKED) idx = min(max(idx, lo_clamp), hi_clamp);
-    xw[q] = chan[idx];
-  }
+  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
 }
 
 // Per-lane pooled state for the kernels of one chunk.
@@ -131,19 +131,33 @@ struct Pool {
   float mx[G];
 };
 
-template <int LEN, int R, int P, bool EXACT, bool MASKED>
-__device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R],
-                                            const float (&thr)[2 * P], int v0, int d, int n,
+// count += (a > thr): FSETP + predicated IADD, both on the ALU pipe (the
+// compiler's own select lowering puts an IMAD.MOV on the FMA pipe).
+__device__ __forceinline__ void count_gt(unsigned& cnt, float a, float thr) {
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(cnt) : "f"(a), "f"(thr));
+}
+__device__ __forceinline__ void count_gt_live(unsigned& cnt, float a, float thr, bool live) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %3, 0;\n\tsetp.gt.and.f32 p, %1, %2, q;\n\t@p add.u32 %0, %0, 1;\n\t}"
+      : "+r"(cnt)
+      : "f"(a), "f"(thr), "r"((unsigned)live));
+}
+
+template <int R, int P, bool MASKED>
+__device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R], const float (&thr)[2 * P],
                                             bool live) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const bool ok = !MASKED || (live && (v0 + r * d < n));
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const float a0 = acc[p][r].x, a1 = acc[p][r].y;
-      if (ok) {
-        st.cnt[2 * p] += (a0 > thr[2 * p]) ? 1u : 0u;
-        st.cnt[2 * p + 1] += (a1 > thr[2 * p + 1]) ? 1u : 0u;
+      if (MASKED) {
+        count_gt_live(st.cnt[2 * p], a0, thr[2 * p], live);
+        count_gt_live(st.cnt[2 * p + 1], a1, thr[2 * p + 1], live);
+        st.mx[2 * p] = live ? fmaxf(st.mx[2 * p], a0) : st.mx[2 * p];
+        st.mx[2 * p + 1] = live ? fmaxf(st.mx[2 * p + 1], a1) : st.mx[2 * p + 1];
+      } else {
+        count_gt(st.cnt[2 * p], a0, thr[2 * p]);
+        count_gt(st.cnt[2 * p + 1], a1, thr[2 * p + 1]);
         st.mx[2 * p] = fmaxf(st.mx[2 * p], a0);
         st.mx[2 * p + 1] = fmaxf(st.mx[2 * p + 1], a1);
       }
@@ -154,8 +168,8 @@ __device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)
 // Finish one chunk: reduce the per-lane pools over the warp and store
 // out[row, col*fpk] = ppv, out[row, col*fpk + 1] = max (engine.py:186-188).
 template <int G, bool EXACT>
-__device__ __forceinline__ void finish_chunk(const DevChunk& c, Pool<G>& st, float* __restrict__ orow,
-                                             int fpk, int vec_out, int lane) {
+__device__ __forceinline__ void finish_chunk(const DevChunk& c, Pool<G>& st, float* __restrict__ orow, int fpk,
+                                             int vec_out, int lane) {
   const double ln = (double)c.n;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -176,15 +190,93 @@ __device__ __forceinline__ void finish_chunk(const DevChunk& c, Pool<G>& st, flo
   }
 }
 
-// One chunk with NC channel slots (NC = 1 or 2, weights resident in
-// registers) — the fast path for every univariate bank.
+// One step: R positions per lane (u0, u0+d, ..., u0+(R-1)d) for P kernel
+// pairs over NC channel slots.  Weights are register-resident (NC*P*LEN
+// float2) or, for the generic channel count, re-read per slot.
+template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
+__device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
+                                           const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
+                                           const float2 (&init)[P], float2 one2, int u0, int d, bool live) {
+  float2 acc[P][R];
+#pragma unroll
+  for (int s = 0; s < NC; ++s) {
+    float xw[R + LEN - 1];
+    load_window<LEN, R>(xw, chan[s], u0, d);
+    if (s == 0) {
+      if (!EXACT) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[p][r] = init[p];
+        accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
+      } else {
+        accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
+      }
+    } else {
+      accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
+    }
+  }
+  pool_update<R, P, MASKED>(st, acc, thr, live);
+}
+
+// Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
+// v = (a*R + r)*d + s, r < R; run starts i = a*d + s are dealt to lanes in
+// consecutive order (conflict-free smem reads: consecutive s -> consecutive
+// addresses, and R odd spreads consecutive a over banks).  Full runs go
+// through unmasked R-position steps; the leftover positions (< 32 run
+// starts plus the final partial run) through masked 1-position steps.
+template <int LEN, int R, int P, int NC, bool EXACT>
+__device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
+                                              const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
+                                              const float2 (&init)[P], float2 one2, int lo, int n, int d,
+                                              int lane) {
+  const int RD = R * d;
+  const int A = n / RD;          // complete runs per residue
+  const int full_starts = A * d;
+  const int nfull = full_starts >> 5;
+  if (nfull > 0) {
+    // incremental (a, s) = divmod(32*step + lane, d)
+    const int q32 = 32 / d, r32 = 32 - q32 * d;
+    int a = lane / d;
+    int s = lane - a * d;
+    int v0 = a * RD + s;
+    const int dv = q32 * RD + r32;
+    for (int stp = 0; stp < nfull; ++stp) {
+      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, true);
+      s += r32;
+      v0 += dv;
+      if (s >= d) {
+        s -= d;
+        v0 += RD - d;
+      }
+    }
+  }
+  const int i0 = nfull << 5;
+  const int m_runs = (full_starts - i0) * R;   // positions of leftover full runs
+  const int m = m_runs + (n - A * RD);         // + the partial last run
+  for (int t0 = 0; t0 < m; t0 += 32) {
+    const int t = t0 + lane;
+    const bool live = t < m;
+    int v;
+    if (t < m_runs) {
+      const int i = i0 + t / R;
+      const int r = t - (t / R) * R;
+      const int a = i / d;
+      v = a * RD + (i - a * d) + r * d;
+    } else {
+      v = A * RD + (t - m_runs);
+    }
+    if (!live) v = 0;
+    chunk_step<LEN, 1, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v, d, live);
+  }
+}
+
+// One chunk, NC channel slots with register-resident weights.
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __restrict__ sx,
-                                       const float* __restrict__ weights, const int* __restrict__ chan_off,
-                                       float* __restrict__ orow, int fpk, int vec_out, int halo, int L,
-                                       float one, int lane) {
+                                          const float* __restrict__ weights, const int* __restrict__ chan_off,
+                                          float* __restrict__ orow, int fpk, int vec_out, float one, int lane) {
   constexpr int G = 2 * P;
-  constexpr int W = R + LEN - 1;
   float2 w[NC][P][LEN];
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
 #pragma unroll
@@ -208,124 +300,54 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
     st.cnt[g] = 0u;
     st.mx[g] = -INFINITY;
   }
-  const float2 one2 = make_float2(one, one);
-  const int d = c.d, n = c.n, lo = c.lo;
-  const int RD = R * d;
-  const int A = n / RD;
-  const int rem = n - A * RD;
-  const int starts = A * d + min(d, rem);
-  const int lo_clamp = -halo, hi_clamp = L + halo - 1;
-  for (int base = 0; base < starts; base += 32) {
-    const int i = base + lane;
-    const bool live = i < starts;
-    const int ii = live ? i : 0;
-    const int a = ii / d;
-    const int s0 = ii - a * d;
-    const int v0 = a * RD + s0;
-    const int u0 = lo + v0;
-    const bool full = __all_sync(kFull, live && (v0 + (R - 1) * d < n));
-    float2 acc[P][R];
-    if (full) {
-#pragma unroll
-      for (int s = 0; s < NC; ++s) {
-        float xw[W];
-        load_window<LEN, R, false>(xw, chan[s], u0, d, lo_clamp, hi_clamp);
-        if (s == 0) {
-          if (!EXACT) {
-#pragma unroll
-            for (int p = 0; p < P; ++p)
-#pragma unroll
-              for (int r = 0; r < R; ++r) acc[p][r] = init[p];
-            accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-          } else {
-            accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
-          }
-        } else {
-          accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-        }
-      }
-      pool_update<LEN, R, P, EXACT, false>(st, acc, thr, v0, d, n, live);
-    } else {
-#pragma unroll
-      for (int s = 0; s < NC; ++s) {
-        float xw[W];
-        load_window<LEN, R, true>(xw, chan[s], u0, d, lo_clamp, hi_clamp);
-        if (s == 0) {
-          if (!EXACT) {
-#pragma unroll
-            for (int p = 0; p < P; ++p)
-#pragma unroll
-              for (int r = 0; r < R; ++r) acc[p][r] = init[p];
-            accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-          } else {
-            accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
-          }
-        } else {
-          accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-        }
-      }
-      pool_update<LEN, R, P, EXACT, true>(st, acc, thr, v0, d, n, live);
-    }
-  }
+  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
-// Generic channel count (>= 3 slots): one kernel pair, weights re-read
-// from L1 per slot and step.
+// Generic channel count (>= 3 slots): one kernel pair, slots looped at run
+// time; the pooled accumulator continues across slots in slot order.
 template <int LEN, int R, bool EXACT>
 __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float* __restrict__ sx,
-                                               const float* __restrict__ weights,
-                                               const int* __restrict__ chan_off, float* __restrict__ orow,
-                                               int fpk, int vec_out, int halo, int L, float one, int lane) {
-  constexpr int P = 1;
-  constexpr int G = 2;
-  constexpr int W = R + LEN - 1;
+                                                  const float* __restrict__ weights,
+                                                  const int* __restrict__ chan_off, float* __restrict__ orow,
+                                                  int fpk, int vec_out, float one, int lane) {
+  // Positions one per lane (R = 1 semantics), window re-read per slot.
+  constexpr int C = (LEN - 1) / 2;
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
-  float thr[G] = {EXACT ? c.thr[0] : 0.0f, EXACT ? c.thr[1] : 0.0f};
+  float thr[2] = {EXACT ? c.thr[0] : 0.0f, EXACT ? c.thr[1] : 0.0f};
   const float2 init = make_float2(c.bias[0], c.bias[1]);
-  Pool<G> st;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    st.cnt[g] = 0u;
-    st.mx[g] = -INFINITY;
-  }
   const float2 one2 = make_float2(one, one);
+  Pool<2> st;
+  st.cnt[0] = st.cnt[1] = 0u;
+  st.mx[0] = st.mx[1] = -INFINITY;
   const int d = c.d, n = c.n, lo = c.lo, nc = c.nc;
-  const int RD = R * d;
-  const int A = n / RD;
-  const int rem = n - A * RD;
-  const int starts = A * d + min(d, rem);
-  const int lo_clamp = -halo, hi_clamp = L + halo - 1;
-  for (int base = 0; base < starts; base += 32) {
-    const int i = base + lane;
-    const bool live = i < starts;
-    const int ii = live ? i : 0;
-    const int a = ii / d;
-    const int s0 = ii - a * d;
-    const int v0 = a * RD + s0;
-    const int u0 = lo + v0;
-    float2 acc[P][R];
+  for (int t0 = 0; t0 < n; t0 += 32) {
+    const int t = t0 + lane;
+    const bool live = t < n;
+    const int u = lo + (live ? t : 0);
+    float2 acc[1][1];
     for (int s = 0; s < nc; ++s) {
-      float2 w[P][LEN];
+      const float* p = sx + __ldg(chan_off + c.chofs + s) + (u - C * d);
+      float xw[LEN];
+#pragma unroll
+      for (int q = 0; q < LEN; ++q) xw[q] = p[q * d];
+      float2 w[1][LEN];
 #pragma unroll
       for (int j = 0; j < LEN; ++j) w[0][j] = __ldg(wp + s * LEN + j);
-      float xw[W];
-      load_window<LEN, R, true>(xw, sx + __ldg(chan_off + c.chofs + s), u0, d, lo_clamp, hi_clamp);
       if (s == 0) {
         if (!EXACT) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[0][r] = init;
-          accumulate<LEN, R, P, EXACT, false>(acc, w, xw, one2);
+          acc[0][0] = init;
+          accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
         } else {
-          accumulate<LEN, R, P, EXACT, true>(acc, w, xw, one2);
+          accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, one2);
         }
       } else {
-        accumulate<LEN, R, P, EXACT, false>(acc, w, xw, one2);
+        accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
       }
     }
-    pool_update<LEN, R, P, EXACT, true>(st, acc, thr, v0, d, n, live);
+    pool_update<1, 1, true>(st, acc, thr, live);
   }
-  finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
+  finish_chunk<2, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
 // One launch per chunk class <LEN, R, NCK>: each class gets its own
@@ -385,11 +407,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
       float* orow = a.out + (series0 + si) * a.ld_out;
       const float* sx = smem + si * slot_floats + H;  // chan_off entries are relative to this
       if (NCK == 0)
-        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, H, L, a.one, lane);
+        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       else if (NCK == 1)
-        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, H, L, a.one, lane);
+        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
+      else if (NCK == 3)
+        run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       else
-        run_chunk_generic<LEN, R, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, H, L, a.one, lane);
+        run_chunk_generic<LEN, R, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
     }
   }
