@@ -60,10 +60,11 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
   const int64_t G = 2 * P;
   const int64_t RD = (int64_t)R * d;
   const int64_t A = n / RD;
+  const int64_t rem = n - A * RD;
   const int64_t full_starts = A * d;
+  const int64_t starts = full_starts + std::min<int64_t>(d, rem);
   const int64_t nfull = full_starts / 32;
-  const int64_t left = (full_starts - nfull * 32) * R + (n - A * RD);
-  const int64_t tail_steps = (left + 31) / 32;
+  const int64_t masked_steps = (starts - nfull * 32 + 31) / 32;
   auto step = [&](int64_t r, int64_t extra) {
     return r * len * nc * P              // FFMA2
            + r * G * 2                   // count (FSETP + IADD)
@@ -71,8 +72,9 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
            + 2 * (r + len - 1) * nc      // window loads + addresses
            + extra;
   };
-  return nfull * step(R, 8) + tail_steps * step(1, 30) + 40 * G + 60;
+  return nfull * step(R, 8) + masked_steps * (step(R, 40) + 2 * (R + len - 1) * nc + R * G) + 40 * G + 60;
 }
+
 }  // namespace
 
 struct rk_bank_s {

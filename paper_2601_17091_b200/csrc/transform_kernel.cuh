@@ -124,6 +124,14 @@ __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const floa
   for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
 }
 
+template <int LEN, int R>
+__device__ __forceinline__ void load_window_clamped(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
+                                                    int u0, int d, int lo_clamp, int hi_clamp) {
+  constexpr int C = (LEN - 1) / 2;
+#pragma unroll
+  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(max(u0 + (q - C) * d, lo_clamp), hi_clamp)];
+}
+
 // Per-lane pooled state for the kernels of one chunk.
 template <int G>
 struct Pool {
@@ -165,6 +173,24 @@ __device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)
   }
 }
 
+// Masked variant: position r of this lane is valid while r*d < nleft.
+template <int R, int P>
+__device__ __forceinline__ void pool_update_masked(Pool<2 * P>& st, const float2 (&acc)[P][R],
+                                                   const float (&thr)[2 * P], bool live, int nleft, int d) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool ok = live && (r * d < nleft);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const float a0 = acc[p][r].x, a1 = acc[p][r].y;
+      count_gt_live(st.cnt[2 * p], a0, thr[2 * p], ok);
+      count_gt_live(st.cnt[2 * p + 1], a1, thr[2 * p + 1], ok);
+      st.mx[2 * p] = ok ? fmaxf(st.mx[2 * p], a0) : st.mx[2 * p];
+      st.mx[2 * p + 1] = ok ? fmaxf(st.mx[2 * p + 1], a1) : st.mx[2 * p + 1];
+    }
+  }
+}
+
 // Finish one chunk: reduce the per-lane pools over the warp and store
 // out[row, col*fpk] = ppv, out[row, col*fpk + 1] = max (engine.py:186-188).
 template <int G, bool EXACT>
@@ -196,12 +222,16 @@ __device__ __forceinline__ void finish_chunk(const DevChunk& c, Pool<G>& st, flo
 template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                           const float2 (&init)[P], float2 one2, int u0, int d, bool live) {
+                                           const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
+                                           int lo_clamp, int hi_clamp, bool live) {
   float2 acc[P][R];
 #pragma unroll
   for (int s = 0; s < NC; ++s) {
     float xw[R + LEN - 1];
-    load_window<LEN, R>(xw, chan[s], u0, d);
+    if (MASKED)
+      load_window_clamped<LEN, R>(xw, chan[s], u0, d, lo_clamp, hi_clamp);
+    else
+      load_window<LEN, R>(xw, chan[s], u0, d);
     if (s == 0) {
       if (!EXACT) {
 #pragma unroll
@@ -216,23 +246,29 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
       accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
     }
   }
-  pool_update<R, P, MASKED>(st, acc, thr, live);
+  if (MASKED)
+    pool_update_masked<R, P>(st, acc, thr, live, nleft, d);
+  else
+    pool_update<R, P, false>(st, acc, thr, true);
 }
 
 // Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
-// v = (a*R + r)*d + s, r < R; run starts i = a*d + s are dealt to lanes in
-// consecutive order (conflict-free smem reads: consecutive s -> consecutive
-// addresses, and R odd spreads consecutive a over banks).  Full runs go
-// through unmasked R-position steps; the leftover positions (< 32 run
-// starts plus the final partial run) through masked 1-position steps.
+// v = (a*R + r)*d + s, r < R, s < d; run starts i = a*d + s are dealt to
+// lanes in consecutive order (consecutive s -> consecutive smem addresses;
+// R odd spreads consecutive a over the banks).  Steps whose 32 starts are
+// all complete runs go through the unmasked path; the remaining starts
+// (incomplete 32-groups and the final partial run, whose positions
+// v0 + r*d may pass n) through one or two masked steps with clamped reads.
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d,
-                                              int lane) {
+                                              int lo_clamp, int hi_clamp, int lane) {
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
+  const int rem = n - A * RD;    // positions of the partial run
   const int full_starts = A * d;
+  const int starts = full_starts + min(d, rem);
   const int nfull = full_starts >> 5;
   if (nfull > 0) {
     // incremental (a, s) = divmod(32*step + lane, d)
@@ -242,7 +278,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     int v0 = a * RD + s;
     const int dv = q32 * RD + r32;
     for (int stp = 0; stp < nfull; ++stp) {
-      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, true);
+      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, 0, true);
       s += r32;
       v0 += dv;
       if (s >= d) {
@@ -251,23 +287,14 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
       }
     }
   }
-  const int i0 = nfull << 5;
-  const int m_runs = (full_starts - i0) * R;   // positions of leftover full runs
-  const int m = m_runs + (n - A * RD);         // + the partial last run
-  for (int t0 = 0; t0 < m; t0 += 32) {
-    const int t = t0 + lane;
-    const bool live = t < m;
-    int v;
-    if (t < m_runs) {
-      const int i = i0 + t / R;
-      const int r = t - (t / R) * R;
-      const int a = i / d;
-      v = a * RD + (i - a * d) + r * d;
-    } else {
-      v = A * RD + (t - m_runs);
-    }
-    if (!live) v = 0;
-    chunk_step<LEN, 1, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v, d, live);
+  for (int base = nfull << 5; base < starts; base += 32) {
+    const int i = base + lane;
+    const bool live = i < starts;
+    const int ii = live ? i : 0;
+    const int a = ii / d;
+    const int v0 = a * RD + (ii - a * d);
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
+                                          live);
   }
 }
 
@@ -275,7 +302,8 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __restrict__ sx,
                                           const float* __restrict__ weights, const int* __restrict__ chan_off,
-                                          float* __restrict__ orow, int fpk, int vec_out, float one, int lane) {
+                                          float* __restrict__ orow, int fpk, int vec_out, float one, int halo,
+                                          int L, int lane) {
   constexpr int G = 2 * P;
   float2 w[NC][P][LEN];
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
@@ -300,7 +328,8 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
     st.cnt[g] = 0u;
     st.mx[g] = -INFINITY;
   }
-  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, lane);
+  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, -halo,
+                                      L + halo - 1, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
@@ -407,11 +436,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
       float* orow = a.out + (series0 + si) * a.ld_out;
       const float* sx = smem + si * slot_floats + H;  // chan_off entries are relative to this
       if (NCK == 0)
-        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
+        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
       else if (NCK == 1)
-        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
+        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
       else if (NCK == 3)
-        run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
+        run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
       else
         run_chunk_generic<LEN, R, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
