@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -230,6 +231,8 @@ bool is_device_pointer(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
+
 // Enqueue the transform of n series already on the device: one launch per
 // non-empty chunk class, all on `stream`.
 int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
@@ -237,6 +240,9 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
   if (n <= 0) return RK_OK;
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
+  // RK_PROFILE=1: time every class launch with events and report on stderr
+  // (diagnostics only; serialises the host on each launch).
+  static const bool profile = getenv("RK_PROFILE") != nullptr;
   const int smem_cap = (int)st->smem_optin - 1024;
   for (int cls = 0; cls < rk::kNumClasses; ++cls) {
     const int nchunks = b->cls_end[cls] - b->cls_begin[cls];
@@ -280,8 +286,30 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
     a.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
     a.one = 1.0f;
     const int64_t grid = std::min<int64_t>(a.n_items, resident);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (profile) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, stream);
+    }
     fn<<<(unsigned)grid, rk::kThreads, smem, stream>>>(a);
     RK_CUDA(cudaGetLastError());
+    if (profile) {
+      cudaEventRecord(e1, stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      int64_t flops = 0;
+      for (int i = b->cls_begin[cls]; i < b->cls_end[cls]; ++i) {
+        const rk::DevChunk& c = b->chunks[i].dev;
+        flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
+      }
+      fprintf(stderr, "RK_PROFILE class len=%d R=%d nck=%d exact=%d chunks=%d spi=%d nb=%d grid=%lld ms=%.3f dense_tflops=%.2f\n",
+              c_len(cls), rk::r_of((cls / rk::kNumNck) % rk::kNumR), cls % rk::kNumNck, exact, nchunks, spi, nb,
+              (long long)grid, ms, flops * (double)n / (ms * 1e-3) / 1e12);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
   }
   return RK_OK;
 }
