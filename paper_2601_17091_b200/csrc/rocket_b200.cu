@@ -231,13 +231,17 @@ bool is_device_pointer(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// per-call device scratch: the executed counter + one item counter per class
+constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * rk::kNumClasses;
+
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
 // Enqueue the transform of n series already on the device: one launch per
 // non-empty chunk class, all on `stream`.
 int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
-           int mode, cudaStream_t stream, unsigned long long* d_exec) {
+           int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
   if (n <= 0) return RK_OK;
+  RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * rk::kNumClasses, stream));
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
   // RK_PROFILE=1: time every class launch with events and report on stderr
@@ -275,6 +279,7 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
     a.chan_off = b->d_chan_off;
     a.block_start = d_bs;
     a.executed = d_exec;
+    a.item_counter = d_counters + cls;
     a.n_blocks = nb;
     a.series_per_item = spi;
     a.n_channels = b->C;
@@ -584,9 +589,10 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     // library's); the executed counter is private to this call.
     cudaStream_t stream = stream_ptr ? (cudaStream_t)stream_ptr : st->stream;
     unsigned long long* d_exec = nullptr;
-    RK_CUDA(cudaMallocAsync(&d_exec, sizeof(unsigned long long), stream));
+    RK_CUDA(cudaMallocAsync(&d_exec, kScratchBytes, stream));
     RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
-    rc = launch(b, st, x, n, out + row0 * ld_out, ld_out, fpk, mode, stream, d_exec);
+    rc = launch(b, st, x, n, out + row0 * ld_out, ld_out, fpk, mode, stream, d_exec,
+                reinterpret_cast<int*>(d_exec + 1));
     if (rc) return rc;
     if (executed) {
       unsigned long long h = 0;
@@ -616,7 +622,7 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
   float* d_o[2] = {nullptr, nullptr};
   unsigned long long* d_exec = nullptr;
   cudaEvent_t ev_done[2];
-  RK_CUDA(cudaMallocAsync(&d_exec, sizeof(unsigned long long), stream));
+  RK_CUDA(cudaMallocAsync(&d_exec, kScratchBytes, stream));
   for (int i = 0; i < 2; ++i) {
     if (!dx) RK_CUDA(cudaMallocAsync(&d_in[i], batch * in_row_bytes, stream));
     if (!dout) RK_CUDA(cudaMallocAsync(&d_o[i], batch * out_row_bytes, stream));
@@ -634,7 +640,7 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     }
     float* ko = dout ? out + (row0 + s0) * ld_out : d_o[k];
     const int64_t kld = dout ? ld_out : b->K * fpk;
-    rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec);
+    rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec, reinterpret_cast<int*>(d_exec + 1));
     if (rc) return rc;
     if (!dout) {
       // D2H on the copy stream so the next batch's kernels can start.

@@ -66,6 +66,7 @@ struct LaunchArgs {
   const int* chan_off;     // device, per chunk slot: smem float offset of channel
   const int* block_start;  // device, n_blocks + 1 chunk boundaries (this class)
   unsigned long long* executed;  // device counter
+  int* item_counter;      // dynamic item scheduler (zeroed before the launch)
   int n_blocks;
   int series_per_item;     // series staged together (small classes)
   int n_channels;
@@ -387,6 +388,7 @@ template <int LEN, int R, int NCK, bool EXACT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(const LaunchArgs a) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_next;
+  __shared__ int s_item;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
@@ -398,13 +400,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
     if (t < H || t >= H + L) smem[k] = 0.0f;
   }
   unsigned long long done = 0;
-  for (int64_t item = blockIdx.x; item < a.n_items; item += gridDim.x) {
+  // Items are claimed dynamically: CTAs of this launch that start late
+  // (while the previous class's tail still occupies SMs) simply take fewer.
+  while (true) {
+    __syncthreads();  // every warp has left the previous item
+    if (tid == 0) s_item = atomicAdd(a.item_counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.n_items) break;
     const int64_t group = item / a.n_blocks;
     const int blk = (int)(item - group * a.n_blocks);
     const int64_t series0 = group * SPI;
     const int64_t left = a.n_series - series0;
     const int ns = left < SPI ? (int)left : SPI;
-    __syncthreads();  // every warp has left the previous item
     const float* xs = a.x + series0 * (int64_t)C * L;
     if (a.vec_in) {
       const int L4 = L >> 2;
