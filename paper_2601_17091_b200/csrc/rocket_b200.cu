@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -247,6 +248,9 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
   // RK_PROFILE=1: time every class launch with events and report on stderr
   // (diagnostics only; serialises the host on each launch).
   static const bool profile = getenv("RK_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> prof_events;
+  std::vector<int> prof_cls;
+  std::vector<std::array<int, 4>> prof_info;
   const int smem_cap = (int)st->smem_optin - 1024;
   for (int cls = 0; cls < rk::kNumClasses; ++cls) {
     const int nchunks = b->cls_end[cls] - b->cls_begin[cls];
@@ -291,30 +295,39 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
     a.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
     a.one = 1.0f;
     const int64_t grid = std::min<int64_t>(a.n_items, resident);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (profile) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0, stream);
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, stream);
+      prof_events.push_back(e);
+      prof_cls.push_back(cls);
+      prof_info.push_back({nchunks, spi, nb, (int)grid});
     }
     fn<<<(unsigned)grid, rk::kThreads, smem, stream>>>(a);
     RK_CUDA(cudaGetLastError());
-    if (profile) {
-      cudaEventRecord(e1, stream);
-      cudaEventSynchronize(e1);
+  }
+  if (profile && !prof_events.empty()) {
+    // events between back-to-back launches (no host sync in between)
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    prof_events.push_back(e);
+    cudaEventSynchronize(e);
+    for (size_t i = 0; i + 1 < prof_events.size(); ++i) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventElapsedTime(&ms, prof_events[i], prof_events[i + 1]);
+      const int cls = prof_cls[i];
       int64_t flops = 0;
-      for (int i = b->cls_begin[cls]; i < b->cls_end[cls]; ++i) {
-        const rk::DevChunk& c = b->chunks[i].dev;
+      for (int k = b->cls_begin[cls]; k < b->cls_end[cls]; ++k) {
+        const rk::DevChunk& c = b->chunks[k].dev;
         flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
       }
-      fprintf(stderr, "RK_PROFILE class len=%d R=%d nck=%d exact=%d chunks=%d spi=%d nb=%d grid=%lld ms=%.3f dense_tflops=%.2f\n",
-              c_len(cls), rk::r_of((cls / rk::kNumNck) % rk::kNumR), cls % rk::kNumNck, exact, nchunks, spi, nb,
-              (long long)grid, ms, flops * (double)n / (ms * 1e-3) / 1e12);
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
+      fprintf(stderr,
+              "RK_PROFILE class len=%d R=%d nck=%d exact=%d chunks=%d spi=%d nb=%d grid=%d ms=%.3f dense_tflops=%.2f\n",
+              c_len(cls), rk::r_of((cls / rk::kNumNck) % rk::kNumR), cls % rk::kNumNck, exact, prof_info[i][0],
+              prof_info[i][1], prof_info[i][2], prof_info[i][3], ms, flops * (double)n / (ms * 1e-3) / 1e12);
     }
+    for (auto ev : prof_events) cudaEventDestroy(ev);
   }
   return RK_OK;
 }
