@@ -47,6 +47,9 @@ int fail(int code, const char* fmt, ...) {
                   __FILE__, __LINE__);                                                 \
   } while (0)
 
+// per-call device scratch: the executed counter + one item counter per class
+constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * rk::kNumClasses;
+
 constexpr int kLenIdx[12] = {-1, -1, -1, -1, -1, -1, -1, 0, -1, 1, -1, 2};
 
 struct HostChunk {
@@ -141,15 +144,31 @@ struct rk_bank_s {
 
 namespace {
 
+// Host-buffer transforms run on a pooled "worker": two streams, two events
+// and double-buffered device scratch, reused across calls (per-call
+// allocation made the stream-ordered pool map and unmap memory every call).
+struct Worker {
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  unsigned long long* d_scratch = nullptr;
+  float* d_in[2] = {nullptr, nullptr};
+  float* d_out[2] = {nullptr, nullptr};
+  size_t in_cap = 0, out_cap = 0;
+};
+
 struct DeviceState {
   int sms = 0;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t copy_stream = nullptr;
   std::map<const void*, int> attr_smem;
+  std::mutex pool_mu;
+  std::vector<Worker*> free_workers;
+  // device-pointer calls: one scratch block per stream (stream order makes
+  // reuse safe)
+  std::map<cudaStream_t, unsigned long long*> stream_scratch;
 };
 std::mutex g_dev_mu;
-std::map<int, DeviceState> g_devs;
+std::map<int, DeviceState*> g_devs;
 
 int device_state(int device, DeviceState** out) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -161,20 +180,19 @@ int device_state(int device, DeviceState** out) {
       return fail(RK_ERR_NO_DEVICE, "no CUDA device is visible");
     }
     if (device < 0 || device >= n) return fail(RK_ERR_INVALID, "device %d out of range [0, %d)", device, n);
-    DeviceState st;
     RK_CUDA(cudaSetDevice(device));
     cudaDeviceProp prop;
     RK_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10)
       return fail(RK_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
                   prop.major, prop.minor);
-    st.sms = prop.multiProcessorCount;
-    st.smem_optin = prop.sharedMemPerBlockOptin;
-    RK_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
-    RK_CUDA(cudaStreamCreateWithFlags(&st.copy_stream, cudaStreamNonBlocking));
+    DeviceState* st = new DeviceState();
+    st->sms = prop.multiProcessorCount;
+    st->smem_optin = prop.sharedMemPerBlockOptin;
+    RK_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
     it = g_devs.emplace(device, st).first;
   }
-  *out = &it->second;
+  *out = it->second;
   return RK_OK;
 }
 
@@ -213,6 +231,41 @@ const KernelTable& kernel_table() {
   return t;
 }
 
+int stream_scratch(DeviceState* st, cudaStream_t stream, unsigned long long** out) {
+  std::lock_guard<std::mutex> lk(st->pool_mu);
+  auto it = st->stream_scratch.find(stream);
+  if (it == st->stream_scratch.end()) {
+    unsigned long long* p = nullptr;
+    RK_CUDA(cudaMalloc(&p, kScratchBytes));
+    it = st->stream_scratch.emplace(stream, p).first;
+  }
+  *out = it->second;
+  return RK_OK;
+}
+
+int acquire_worker(DeviceState* st, Worker** out) {
+  {
+    std::lock_guard<std::mutex> lk(st->pool_mu);
+    if (!st->free_workers.empty()) {
+      *out = st->free_workers.back();
+      st->free_workers.pop_back();
+      return RK_OK;
+    }
+  }
+  Worker* w = new Worker();
+  RK_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+  RK_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&w->ev[i], cudaEventDisableTiming));
+  RK_CUDA(cudaMalloc(&w->d_scratch, kScratchBytes));
+  *out = w;
+  return RK_OK;
+}
+
+void release_worker(DeviceState* st, Worker* w) {
+  std::lock_guard<std::mutex> lk(st->pool_mu);
+  st->free_workers.push_back(w);
+}
+
 int set_kernel_smem(DeviceState* st, KernelFn fn, int bytes) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   auto it = st->attr_smem.find((const void*)fn);
@@ -231,9 +284,6 @@ bool is_device_pointer(const void* p) {
   }
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
-
-// per-call device scratch: the executed counter + one item counter per class
-constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * rk::kNumClasses;
 
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
@@ -599,10 +649,11 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
   const int64_t row_in = (int64_t)b->C * b->L;
   if (dx && dout) {
     // Device-resident: asynchronous on the caller's stream (or the
-    // library's); the executed counter is private to this call.
+    // library's); the counters live in that stream's scratch block.
     cudaStream_t stream = stream_ptr ? (cudaStream_t)stream_ptr : st->stream;
     unsigned long long* d_exec = nullptr;
-    RK_CUDA(cudaMallocAsync(&d_exec, kScratchBytes, stream));
+    rc = stream_scratch(st, stream, &d_exec);
+    if (rc) return rc;
     RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
     rc = launch(b, st, x, n, out + row0 * ld_out, ld_out, fpk, mode, stream, d_exec,
                 reinterpret_cast<int*>(d_exec + 1));
@@ -610,37 +661,53 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     if (executed) {
       unsigned long long h = 0;
       RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));
-      RK_CUDA(cudaFreeAsync(d_exec, stream));
       RK_CUDA(cudaStreamSynchronize(stream));
       *executed = (int64_t)h;
-    } else {
-      RK_CUDA(cudaFreeAsync(d_exec, stream));
     }
     return RK_OK;
   }
-  // Host buffers: row batches through device scratch on two private
-  // streams (reentrant per call), double-buffered so batch i+1's H2D and
-  // batch i-1's D2H overlap batch i's kernels.
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
-  RK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  RK_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  // Host buffers: row batches through a pooled worker's device buffers,
+  // double-buffered so batch i+1's H2D and batch i-1's D2H overlap batch
+  // i's kernels.
+  Worker* w = nullptr;
+  rc = acquire_worker(st, &w);
+  if (rc) return rc;
+  struct Release {
+    DeviceState* st;
+    Worker* w;
+    ~Release() { release_worker(st, w); }
+  } release{st, w};
+  cudaStream_t stream = w->stream, copy_stream = w->copy_stream;
   const int64_t out_row_bytes = b->K * fpk * 4;
   const int64_t in_row_bytes = row_in * 4;
   const int64_t budget = (int64_t)1 << 30;  // device scratch per buffer
   int64_t batch = std::max<int64_t>(1, budget / (out_row_bytes + in_row_bytes));
   batch = std::min<int64_t>(batch, n);
-  // at least two batches in flight when there is enough work to overlap
+  // at least four batches when there is enough work to overlap copies
   if (n >= 4096) batch = std::min<int64_t>(batch, (n + 3) / 4);
-  float* d_in[2] = {nullptr, nullptr};
-  float* d_o[2] = {nullptr, nullptr};
-  unsigned long long* d_exec = nullptr;
-  cudaEvent_t ev_done[2];
-  RK_CUDA(cudaMallocAsync(&d_exec, kScratchBytes, stream));
-  for (int i = 0; i < 2; ++i) {
-    if (!dx) RK_CUDA(cudaMallocAsync(&d_in[i], batch * in_row_bytes, stream));
-    if (!dout) RK_CUDA(cudaMallocAsync(&d_o[i], batch * out_row_bytes, stream));
-    RK_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  if (!dx) {
+    const size_t need = (size_t)(batch * in_row_bytes);
+    if (need > w->in_cap) {
+      for (int i = 0; i < 2; ++i) {
+        if (w->d_in[i]) RK_CUDA(cudaFree(w->d_in[i]));
+        w->d_in[i] = nullptr;
+        RK_CUDA(cudaMalloc(&w->d_in[i], need));
+      }
+      w->in_cap = need;
+    }
   }
+  if (!dout) {
+    const size_t need = (size_t)(batch * out_row_bytes);
+    if (need > w->out_cap) {
+      for (int i = 0; i < 2; ++i) {
+        if (w->d_out[i]) RK_CUDA(cudaFree(w->d_out[i]));
+        w->d_out[i] = nullptr;
+        RK_CUDA(cudaMalloc(&w->d_out[i], need));
+      }
+      w->out_cap = need;
+    }
+  }
+  unsigned long long* d_exec = w->d_scratch;
   RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
   int64_t bi = 0;
   for (int64_t s0 = 0; s0 < n; s0 += batch, ++bi) {
@@ -648,41 +715,33 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     const int k = (int)(bi & 1);
     const float* kx = x + s0 * row_in;
     if (!dx) {
-      RK_CUDA(cudaMemcpyAsync(d_in[k], kx, cnt * in_row_bytes, cudaMemcpyHostToDevice, stream));
-      kx = d_in[k];
+      RK_CUDA(cudaMemcpyAsync(w->d_in[k], kx, cnt * in_row_bytes, cudaMemcpyHostToDevice, stream));
+      kx = w->d_in[k];
     }
-    float* ko = dout ? out + (row0 + s0) * ld_out : d_o[k];
+    float* ko = dout ? out + (row0 + s0) * ld_out : w->d_out[k];
     const int64_t kld = dout ? ld_out : b->K * fpk;
     rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec, reinterpret_cast<int*>(d_exec + 1));
     if (rc) return rc;
     if (!dout) {
       // D2H on the copy stream so the next batch's kernels can start.
-      RK_CUDA(cudaEventRecord(ev_done[k], stream));
-      RK_CUDA(cudaStreamWaitEvent(copy_stream, ev_done[k], 0));
+      RK_CUDA(cudaEventRecord(w->ev[k], stream));
+      RK_CUDA(cudaStreamWaitEvent(copy_stream, w->ev[k], 0));
       float* hdst = out + (row0 + s0) * ld_out;
       if (ld_out == kld) {
-        RK_CUDA(cudaMemcpyAsync(hdst, d_o[k], cnt * out_row_bytes, cudaMemcpyDeviceToHost, copy_stream));
+        RK_CUDA(cudaMemcpyAsync(hdst, w->d_out[k], cnt * out_row_bytes, cudaMemcpyDeviceToHost, copy_stream));
       } else {
-        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, d_o[k], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
+        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, w->d_out[k], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
                                   copy_stream));
       }
       // the next use of buffer k waits for this copy
-      RK_CUDA(cudaEventRecord(ev_done[k], copy_stream));
-      RK_CUDA(cudaStreamWaitEvent(stream, ev_done[k], 0));
+      RK_CUDA(cudaEventRecord(w->ev[k], copy_stream));
+      RK_CUDA(cudaStreamWaitEvent(stream, w->ev[k], 0));
     }
   }
   unsigned long long h = 0;
   RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));
   RK_CUDA(cudaStreamSynchronize(copy_stream));
-  for (int i = 0; i < 2; ++i) {
-    if (d_in[i]) RK_CUDA(cudaFreeAsync(d_in[i], stream));
-    if (d_o[i]) RK_CUDA(cudaFreeAsync(d_o[i], stream));
-  }
-  RK_CUDA(cudaFreeAsync(d_exec, stream));
   RK_CUDA(cudaStreamSynchronize(stream));
-  for (int i = 0; i < 2; ++i) cudaEventDestroy(ev_done[i]);
-  cudaStreamDestroy(stream);
-  cudaStreamDestroy(copy_stream);
   if (executed) *executed = (int64_t)h;
   return RK_OK;
 }
@@ -765,9 +824,29 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, c
 }
 
 int rk_release_caches(void) {
-  std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto& kv : g_cache) rk_bank_destroy(kv.second);
-  g_cache.clear();
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto& kv : g_cache) rk_bank_destroy(kv.second);
+    g_cache.clear();
+  }
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  for (auto& kv : g_devs) {
+    DeviceState* st = kv.second;
+    cudaSetDevice(kv.first);
+    std::lock_guard<std::mutex> pl(st->pool_mu);
+    for (Worker* w : st->free_workers) {
+      for (int i = 0; i < 2; ++i) {
+        cudaFree(w->d_in[i]);
+        cudaFree(w->d_out[i]);
+        cudaEventDestroy(w->ev[i]);
+      }
+      cudaFree(w->d_scratch);
+      cudaStreamDestroy(w->stream);
+      cudaStreamDestroy(w->copy_stream);
+      delete w;
+    }
+    st->free_workers.clear();
+  }
   return RK_OK;
 }
 
