@@ -11,7 +11,7 @@ import sys
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "_build", "librocket_b200.so")
+LIB_PATH = os.environ.get("RK_LIB_PATH") or os.path.join(_PKG, "_build", "librocket_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -65,15 +65,17 @@ class BankInfo(ctypes.Structure):
     ]
 
 
-def build(verbose=False):
+def build(verbose=False, out=None, defines=()):
     """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles
     without a GPU)."""
-    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH, os.path.join(CSRC, "rocket_b200.cu")]
+    out = out or LIB_PATH
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", out,
+           os.path.join(CSRC, "rocket_b200.cu")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    return LIB_PATH
+    return out
 
 
 _lib = None

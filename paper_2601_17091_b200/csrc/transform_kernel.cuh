@@ -22,8 +22,17 @@
 
 namespace rk {
 
-constexpr int kThreads = 256;      // 8 warps per CTA
-constexpr int kMinBlocks = 2;      // 2 CTAs / SM  -> <= 128 registers
+#ifndef RK_THREADS
+#define RK_THREADS 256
+#endif
+#ifndef RK_MINBLOCKS
+#define RK_MINBLOCKS 2
+#endif
+#ifndef RK_RSTEP
+#define RK_RSTEP 2
+#endif
+constexpr int kThreads = RK_THREADS;      // 8 warps per CTA
+constexpr int kMinBlocks = RK_MINBLOCKS;  // 2 CTAs / SM  -> <= 128 registers
 constexpr int kChunkKernels = 4;   // kernels per chunk (2 FFMA2 pairs)
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -31,7 +40,8 @@ constexpr unsigned kFull = 0xffffffffu;
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
 //           2: >= 3 channels (generic); 3: 1 channel, 1 pair
 constexpr int kNumR = 4;
-__host__ __device__ constexpr int r_of(int r_idx) { return 2 * r_idx + 1; }  // 1,3,5,7
+// positions per lane of class r_idx: 1,3,5,7 (RK_RSTEP 2) or 1,4,7,10 (3)
+__host__ __device__ constexpr int r_of(int r_idx) { return RK_RSTEP * r_idx + 1; }
 constexpr int kNumNck = 4;
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
