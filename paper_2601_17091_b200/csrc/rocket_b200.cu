@@ -48,7 +48,8 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // per-call device scratch: the executed counter + one item counter per class
-constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * rk::kNumClasses;
+constexpr int kMaxLaunches = 1024;
+constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * kMaxLaunches;
 
 constexpr int kLenIdx[12] = {-1, -1, -1, -1, -1, -1, -1, 0, -1, 1, -1, 2};
 
@@ -96,6 +97,16 @@ struct rk_bank_s {
   std::vector<int64_t> cost_prefix;
   int cls_begin[rk::kNumClasses] = {};
   int cls_end[rk::kNumClasses] = {};
+  // warp path (short series): per-launch parameter blocks, built once
+  struct WarpLaunch {
+    int cls;
+    int n_chunks;
+    int64_t dense_flops;  // 2 * taps * positions of one series (diagnostics)
+    std::vector<rk::float4_t> blob;
+  };
+  bool warp_path = false;
+  int warp_ctas_per_sm = 0;
+  std::vector<WarpLaunch> warp_launches;
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
   int* d_chan_off = nullptr;
@@ -266,6 +277,38 @@ void release_worker(DeviceState* st, Worker* w) {
   st->free_workers.push_back(w);
 }
 
+// Warp-path kernel table: (class, mode) -> rocket_warp_kernel instance.
+using WarpFn = void (*)(const rk::WParams);
+template <int LEN, int R>
+void wfill_nck(WarpFn* t, int li, int ri) {
+  const int base = (li * rk::kNumR + ri) * rk::kNumNck;
+  t[2 * (base + 0) + 0] = rk::rocket_warp_kernel<LEN, R, 2, 1, false>;
+  t[2 * (base + 0) + 1] = rk::rocket_warp_kernel<LEN, R, 2, 1, true>;
+  t[2 * (base + 1) + 0] = rk::rocket_warp_kernel<LEN, R, 1, 2, false>;
+  t[2 * (base + 1) + 1] = rk::rocket_warp_kernel<LEN, R, 1, 2, true>;
+  t[2 * (base + 3) + 0] = rk::rocket_warp_kernel<LEN, R, 1, 1, false>;
+  t[2 * (base + 3) + 1] = rk::rocket_warp_kernel<LEN, R, 1, 1, true>;
+}
+template <int LEN>
+void wfill_r(WarpFn* t, int li) {
+  wfill_nck<LEN, rk::r_of(0)>(t, li, 0);
+  wfill_nck<LEN, rk::r_of(1)>(t, li, 1);
+  wfill_nck<LEN, rk::r_of(2)>(t, li, 2);
+  wfill_nck<LEN, rk::r_of(3)>(t, li, 3);
+}
+struct WarpTable {
+  WarpFn fn[2 * rk::kNumClasses] = {};
+  WarpTable() {
+    wfill_r<7>(fn, 0);
+    wfill_r<9>(fn, 1);
+    wfill_r<11>(fn, 2);
+  }
+};
+const WarpTable& warp_table() {
+  static WarpTable t;
+  return t;
+}
+
 int set_kernel_smem(DeviceState* st, KernelFn fn, int bytes) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   auto it = st->attr_smem.find((const void*)fn);
@@ -289,10 +332,88 @@ int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
 // Enqueue the transform of n series already on the device: one launch per
 // non-empty chunk class, all on `stream`.
+// Warp path: one PDL-chained launch per parameter block.
+int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
+                int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
+  const int exact = mode == RK_MODE_EXACT ? 1 : 0;
+  static const bool profile = getenv("RK_PROFILE") != nullptr;
+  static rk::WParams params;  // 32 KB: kept off the stack; guarded by the caller's lock
+  static std::mutex params_mu;
+  std::lock_guard<std::mutex> lk(params_mu);
+  const int smem = b->smem_bytes;
+  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * b->warp_ctas_per_sm);
+  std::vector<cudaEvent_t> evs;
+  for (size_t li = 0; li < b->warp_launches.size(); ++li) {
+    const auto& wl = b->warp_launches[li];
+    WarpFn fn = warp_table().fn[2 * wl.cls + exact];
+    if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
+    int rc = set_kernel_smem(st, (KernelFn)fn, smem);
+    if (rc) return rc;
+    const int nck = wl.cls % rk::kNumNck;
+    const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
+    const int len = c_len(wl.cls);
+    rk::WHeader& h = params.h;
+    h.x = d_x;
+    h.out = d_out;
+    h.executed = d_exec;
+    h.item_counter = d_counters + li;
+    h.ld_out = ld_out;
+    h.n_series = n;
+    h.n_chunks = wl.n_chunks;
+    h.l_series = b->L;
+    h.n_channels = b->C;
+    h.halo = b->halo;
+    h.sstride = b->sstride;
+    h.fpk = fpk;
+    h.vec_out = (fpk == 2 && (ld_out % 2) == 0 && ((uintptr_t)d_out % 8) == 0) ? 1 : 0;
+    h.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
+    h.one = 1.0f;
+    h.wbytes = NC * P * len * 8;
+    std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = li == 0 ? 0 : 1;  // the first launch follows the counter memset normally
+    if (profile) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, stream);
+      evs.push_back(e);
+      cfg.numAttrs = 0;
+    }
+    void* args[] = {&params};
+    RK_CUDA(cudaLaunchKernelExC(&cfg, (const void*)fn, args));
+  }
+  if (profile) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    evs.push_back(e);
+    cudaEventSynchronize(e);
+    for (size_t i = 0; i + 1 < evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
+      const auto& wl = b->warp_launches[i];
+      fprintf(stderr, "RK_PROFILE warp len=%d R=%d nck=%d exact=%d chunks=%d grid=%lld ms=%.3f dense_tflops=%.2f\n",
+              c_len(wl.cls), rk::r_of((wl.cls / rk::kNumNck) % rk::kNumR), wl.cls % rk::kNumNck, exact,
+              wl.n_chunks, (long long)grid, ms, wl.dense_flops * (double)n / (ms * 1e-3) / 1e12);
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+  return RK_OK;
+}
+
 int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
            int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
   if (n <= 0) return RK_OK;
-  RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * rk::kNumClasses, stream));
+  RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
+  if (b->warp_path) return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
   // RK_PROFILE=1: time every class launch with events and report on stderr
@@ -592,6 +713,61 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   b->cost_prefix.assign(b->chunks.size() + 1, 0);
   for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
 
+  // Warp path: every chunk has <= 2 channel slots and 24 one-warp CTAs
+  // (each with its own staged series) fit in an SM's shared memory.
+  {
+    const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
+    const int ctas = std::min<int>(rk::kWarpCtasPerSm, (int)((st->smem_optin + 1024) / per_cta));
+    bool ok = ctas >= 12 && !getenv("RK_NO_WARP_PATH");
+    for (auto& hc : b->chunks) ok = ok && (hc.dev.cls % rk::kNumNck) != 2;
+    if (ok) {
+      b->warp_path = true;
+      b->warp_ctas_per_sm = ctas;
+      for (int cls = 0; cls < rk::kNumClasses; ++cls) {
+        const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
+        if (ce <= cb) continue;
+        const int nck = cls % rk::kNumNck;
+        const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
+        const int len = 7 + 2 * (cls / (rk::kNumNck * rk::kNumR));
+        const int wbytes = NC * P * len * 8;
+        const int per_chunk = (int)sizeof(rk::WChunk) + wbytes;
+        const int cap = (rk::kBlobFloat4 * 16) / per_chunk;
+        for (int i0 = cb; i0 < ce; i0 += cap) {
+          const int nch = std::min(cap, ce - i0);
+          rk_bank_s::WarpLaunch wl;
+          wl.cls = cls;
+          wl.n_chunks = nch;
+          wl.dense_flops = 0;
+          wl.blob.assign(rk::kBlobFloat4, rk::float4_t{0, 0, 0, 0});
+          char* raw = reinterpret_cast<char*>(wl.blob.data());
+          for (int j = 0; j < nch; ++j) {
+            const rk::DevChunk& c = b->chunks[i0 + j].dev;
+            rk::WChunk wc;
+            std::memset(&wc, 0, sizeof(wc));
+            wc.d = c.d;
+            wc.lo = c.lo;
+            wc.n = c.n;
+            wc.nk = c.nk;
+            for (int g = 0; g < 4; ++g) {
+              wc.col[g] = c.col[g];
+              wc.bias[g] = c.bias[g];
+              wc.thr[g] = c.thr[g];
+            }
+            for (int s2 = 0; s2 < NC; ++s2) wc.ch[s2] = chan_off[c.chofs + s2] / (int)sstride;
+            std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
+            std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
+            wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
+          }
+          b->warp_launches.push_back(std::move(wl));
+        }
+      }
+      if ((int)b->warp_launches.size() > kMaxLaunches) {
+        b->warp_path = false;
+        b->warp_launches.clear();
+      }
+    }
+  }
+
   std::vector<rk::DevChunk> dev(b->chunks.size());
   for (size_t i = 0; i < b->chunks.size(); ++i) dev[i] = b->chunks[i].dev;
   if (wpack.empty()) wpack.push_back(0.0f);
@@ -627,7 +803,10 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
-  for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;
+  if (b->warp_path)
+    info->n_launches = (int32_t)b->warp_launches.size();
+  else
+    for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;
   return RK_OK;
 }
 

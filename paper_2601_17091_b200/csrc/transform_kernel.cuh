@@ -204,8 +204,8 @@ __device__ __forceinline__ void pool_update_masked(Pool<2 * P>& st, const float2
 
 // Finish one chunk: reduce the per-lane pools over the warp and store
 // out[row, col*fpk] = ppv, out[row, col*fpk + 1] = max (engine.py:186-188).
-template <int G, bool EXACT>
-__device__ __forceinline__ void finish_chunk(const DevChunk& c, Pool<G>& st, float* __restrict__ orow, int fpk,
+template <int G, bool EXACT, class CH>
+__device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __restrict__ orow, int fpk,
                                              int vec_out, int lane) {
   const double ln = (double)c.n;
 #pragma unroll
@@ -465,6 +465,126 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
     }
   }
   if (lane == 0 && done) atomicAdd(a.executed, done);
+}
+
+// ---------------------------------------------------------------------------
+// Warp path (short series): one warp per CTA, 24 CTAs per SM.  The chunk
+// descriptors and weights of one launch travel in the kernel's
+// __grid_constant__ parameter block (<= 32 KB); the chunk loop counter is
+// warp-uniform, so ptxas keeps the weights in uniform registers (LDCU) and
+// FFMA2 reads them as UR operands — ~60 vector registers instead of ~120,
+// hence 1.5x the resident warps of the class kernel.  Each CTA stages its
+// own copy of the series (C * sstride floats) and claims series dynamically.
+constexpr int kWarpCtasPerSm = 24;
+struct float4_t {  // host-side storage of the parameter blob
+  float x, y, z, w;
+};
+constexpr int kParamBytes = 32000;
+
+struct __align__(16) WChunk {  // 80 bytes
+  int d, lo, n, nk;
+  int col[4];
+  float bias[4];
+  float thr[4];
+  int ch[2];  // channel slots (smem offsets are ch * sstride)
+  int pad_[2];
+};
+static_assert(sizeof(WChunk) == 80, "WChunk layout");
+
+struct WHeader {
+  const float* x;
+  float* out;
+  unsigned long long* executed;
+  int* item_counter;
+  int64_t ld_out;
+  int64_t n_series;
+  int n_chunks;
+  int l_series;
+  int n_channels;
+  int halo;
+  int sstride;
+  int fpk;
+  int vec_out;
+  int vec_in;
+  float one;
+  int wbytes;  // bytes of weights per chunk
+};
+constexpr int kBlobFloat4 = (kParamBytes - (int)sizeof(WHeader)) / 16;
+struct WParams {
+  WHeader h;
+  float4 blob[kBlobFloat4];  // n_chunks WChunk, then n_chunks weight blocks
+};
+
+template <int LEN, int R, int P, int NC, bool EXACT>
+__global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const __grid_constant__ WParams p) {
+  extern __shared__ __align__(16) float smem[];
+  // the next class launch (PDL) may start filling SMs as this one drains;
+  // launches of one transform are independent (disjoint output columns)
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int lane = threadIdx.x;
+  const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
+  for (int k = lane; k < C * S; k += 32) {
+    const int t = k % S;
+    if (t < H || t >= H + L) smem[k] = 0.0f;
+  }
+  const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
+  const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
+  const float* sx = smem + H;
+  const float2 one2 = make_float2(p.h.one, p.h.one);
+  unsigned long long done = 0;
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(p.h.item_counter, 1);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= p.h.n_series) break;
+    __syncwarp();
+    const float* xs = p.h.x + (int64_t)item * C * L;
+    if (p.h.vec_in) {
+      const int L4 = L >> 2;
+      for (int k = lane; k < C * L4; k += 32) {
+        const int ch = k / L4, t = k - ch * L4;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)ch * L) + t);
+        *reinterpret_cast<float4*>(smem + ch * S + H + 4 * t) = v;
+      }
+    } else {
+      for (int k = lane; k < C * L; k += 32) {
+        const int ch = k / L, t = k - ch * L;
+        smem[ch * S + H + t] = __ldg(xs + k);
+      }
+    }
+    __syncwarp();
+    float* orow = p.h.out + (int64_t)item * p.h.ld_out;
+    for (int ci = 0; ci < p.h.n_chunks; ++ci) {
+      const WChunk& c = chunks[ci];
+      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
+      float2 w[NC][P][LEN];
+#pragma unroll
+      for (int s = 0; s < NC; ++s)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
+      const float* chan[NC];
+#pragma unroll
+      for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+      float thr[2 * P];
+      float2 init[P];
+#pragma unroll
+      for (int g = 0; g < 2 * P; ++g) thr[g] = EXACT ? c.thr[g] : 0.0f;
+#pragma unroll
+      for (int q = 0; q < P; ++q) init[q] = make_float2(c.bias[2 * q], c.bias[2 * q + 1]);
+      Pool<2 * P> st;
+#pragma unroll
+      for (int g = 0; g < 2 * P; ++g) {
+        st.cnt[g] = 0u;
+        st.mx[g] = -INFINITY;
+      }
+      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
+      finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
+      done += (unsigned long long)c.nk * (unsigned long long)c.n;
+    }
+  }
+  if (lane == 0 && done) atomicAdd(p.h.executed, done);
 }
 
 }  // namespace rk
