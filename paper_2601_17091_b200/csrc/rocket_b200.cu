@@ -691,11 +691,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       k0 += nk;
     }
   }
-  // thresholds depend on the mode only through the sign convention; the
-  // exact kernel compares acc > -bias, the fast kernel acc(+bias) > 0.
-  // Both are stored: thr holds -bias and the fast kernel ignores it.
-  // exact: count acc > -bias (RN(acc + b) > 0 <=> acc > -b); "+ 0.0f"
-  // keeps the threshold off -0 (the kernel's compare is a plain setp.gt).
+  // Both modes accumulate the taps without the bias and count acc > -bias
+  // (RN(acc + b) > 0 <=> acc > -b exactly); "+ 0.0f" keeps the threshold
+  // off -0 (the kernel's compare is a plain setp.gt).
   for (auto& hc : b->chunks)
     for (int g = 0; g < 4; ++g) hc.dev.thr[g] = -hc.dev.bias[g] + 0.0f;
   // class-major order (keeps the warps of a CTA in one code path), then

@@ -60,8 +60,8 @@ struct __align__(16) DevChunk {
   int chofs;  // offset into the channel-slot table (smem offsets)
   int pad_[3];
   int col[4];     // bank index of each kernel slot
-  float thr[4];   // count threshold: exact -> -bias, fast -> 0
-  float bias[4];  // exact: added to the max at the end; fast: acc init
+  float thr[4];   // count threshold: -bias (+0.0f, never -0)
+  float bias[4];  // added to the pooled max at the end (both modes)
 };
 static_assert(sizeof(DevChunk) == 96, "DevChunk layout");
 
@@ -103,7 +103,10 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // Accumulate one channel slot of a window into acc for P kernel pairs.
 // EXACT: acc = RN(acc + RN(w*x)) per tap (FMUL2, then FFMA2 with an opaque
-// 1.0 so the product is rounded on its own; reference.py:7-16).
+// 1.0 so the product is rounded on its own; reference.py:7-16).  FAST: one
+// FFMA2 per tap pair.  Both start from the first product (no bias in the
+// accumulator: the pooling compares against -bias and adds the bias to the
+// max at the end, RN(acc + b) > 0 <=> acc > -b).
 template <int LEN, int R, int P, bool EXACT, bool FIRST>
 __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w)[P][LEN],
                                            const float (&xw)[R + LEN - 1], float2 one2) {
@@ -114,10 +117,10 @@ __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const float2 xv = make_float2(xw[r + j], xw[r + j]);
-        if (EXACT) {
-          const float2 prod = fmul2(w[p][j], xv);
-          if (FIRST && j == 0) acc[p][r] = prod;
-          else acc[p][r] = ffma2(prod, one2, acc[p][r]);
+        if (FIRST && j == 0) {
+          acc[p][r] = fmul2(w[p][j], xv);  // first tap: RN(w*x) == RN(+0 + RN(w*x))
+        } else if (EXACT) {
+          acc[p][r] = ffma2(fmul2(w[p][j], xv), one2, acc[p][r]);
         } else {
           acc[p][r] = ffma2(w[p][j], xv, acc[p][r]);
         }
@@ -207,22 +210,33 @@ __device__ __forceinline__ void pool_update_masked(Pool<2 * P>& st, const float2
 template <int G, bool EXACT, class CH>
 __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __restrict__ orow, int fpk,
                                              int vec_out, int lane) {
-  const double ln = (double)c.n;
+  // reduce every kernel over the warp, then lane g finishes kernel g (one
+  // float64 division per lane in parallel instead of G divergent ones)
+  unsigned my_cnt = 0;
+  float my_max = -INFINITY, my_bias = 0.0f;
+  int my_col = 0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const unsigned tot = __reduce_add_sync(kFull, st.cnt[g]);
     const float m = warp_max(st.mx[g]);
-    if (lane == g && g < c.nk) {
-      // ppv: count / l_out divided in float64, stored as float32 (engine.py:187)
-      const float ppv = __double2float_rn(__ddiv_rn((double)tot, ln));
-      const float mx = EXACT ? __fadd_rn(m, c.bias[g]) : m;
-      float* dst = orow + (int64_t)c.col[g] * fpk;
-      if (vec_out) {
-        *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
-      } else {
-        dst[0] = ppv;
-        dst[1] = mx;
-      }
+    if (lane == g) {
+      my_cnt = tot;
+      my_max = m;
+      my_bias = c.bias[g];
+      my_col = c.col[g];
+    }
+  }
+  if (lane < c.nk) {
+    // ppv: count / l_out divided in float64, stored as float32 (engine.py:187)
+    const float ppv = __double2float_rn(__ddiv_rn((double)my_cnt, (double)c.n));
+    // max: RN(max_t acc_t + b) == max_t RN(acc_t + b) (RN(. + b) is monotone)
+    const float mx = __fadd_rn(my_max, my_bias);
+    float* dst = orow + (int64_t)my_col * fpk;
+    if (vec_out) {
+      *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
+    } else {
+      dst[0] = ppv;
+      dst[1] = mx;
     }
   }
 }
@@ -233,7 +247,7 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
 template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                           const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
+                                           float2 one2, int u0, int d, int nleft,
                                            int lo_clamp, int hi_clamp, bool live) {
   float2 acc[P][R];
 #pragma unroll
@@ -244,15 +258,7 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
     else
       load_window<LEN, R>(xw, chan[s], u0, d);
     if (s == 0) {
-      if (!EXACT) {
-#pragma unroll
-        for (int p = 0; p < P; ++p)
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[p][r] = init[p];
-        accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-      } else {
-        accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
-      }
+      accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
     } else {
       accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
     }
@@ -273,7 +279,7 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                              const float2 (&init)[P], float2 one2, int lo, int n, int d,
+                                              float2 one2, int lo, int n, int d,
                                               int lo_clamp, int hi_clamp, int lane) {
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
@@ -289,7 +295,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     int v0 = a * RD + s;
     const int dv = q32 * RD + r32;
     for (int stp = 0; stp < nfull; ++stp) {
-      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, 0, true);
+      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, one2, lo + v0, d, n, 0, 0, true);
       s += r32;
       v0 += dv;
       if (s >= d) {
@@ -304,7 +310,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     const int ii = live ? i : 0;
     const int a = ii / d;
     const int v0 = a * RD + (ii - a * d);
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
                                           live);
   }
 }
@@ -328,18 +334,15 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
 #pragma unroll
   for (int s = 0; s < NC; ++s) chan[s] = sx + __ldg(chan_off + c.chofs + s);
   float thr[G];
-  float2 init[P];
 #pragma unroll
-  for (int g = 0; g < G; ++g) thr[g] = EXACT ? c.thr[g] : 0.0f;
-#pragma unroll
-  for (int p = 0; p < P; ++p) init[p] = make_float2(c.bias[2 * p], c.bias[2 * p + 1]);
+  for (int g = 0; g < G; ++g) thr[g] = c.thr[g];
   Pool<G> st;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     st.cnt[g] = 0u;
     st.mx[g] = -INFINITY;
   }
-  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, -halo,
+  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, make_float2(one, one), c.lo, c.n, c.d, -halo,
                                       L + halo - 1, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
@@ -354,8 +357,7 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
   // Positions one per lane (R = 1 semantics), window re-read per slot.
   constexpr int C = (LEN - 1) / 2;
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
-  float thr[2] = {EXACT ? c.thr[0] : 0.0f, EXACT ? c.thr[1] : 0.0f};
-  const float2 init = make_float2(c.bias[0], c.bias[1]);
+  float thr[2] = {c.thr[0], c.thr[1]};
   const float2 one2 = make_float2(one, one);
   Pool<2> st;
   st.cnt[0] = st.cnt[1] = 0u;
@@ -375,12 +377,7 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
 #pragma unroll
       for (int j = 0; j < LEN; ++j) w[0][j] = __ldg(wp + s * LEN + j);
       if (s == 0) {
-        if (!EXACT) {
-          acc[0][0] = init;
-          accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
-        } else {
-          accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, one2);
-        }
+        accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, one2);
       } else {
         accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
       }
@@ -568,18 +565,15 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
 #pragma unroll
       for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
       float thr[2 * P];
-      float2 init[P];
 #pragma unroll
-      for (int g = 0; g < 2 * P; ++g) thr[g] = EXACT ? c.thr[g] : 0.0f;
-#pragma unroll
-      for (int q = 0; q < P; ++q) init[q] = make_float2(c.bias[2 * q], c.bias[2 * q + 1]);
+      for (int g = 0; g < 2 * P; ++g) thr[g] = c.thr[g];
       Pool<2 * P> st;
 #pragma unroll
       for (int g = 0; g < 2 * P; ++g) {
         st.cnt[g] = 0u;
         st.mx[g] = -INFINITY;
       }
-      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
+      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
       finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
     }
