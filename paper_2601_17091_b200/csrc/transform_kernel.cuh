@@ -28,9 +28,13 @@ namespace rk {
 #ifndef RK_MINBLOCKS
 #define RK_MINBLOCKS 2
 #endif
-#ifndef RK_RSTEP
-#define RK_RSTEP 2
+#ifndef RK_RMAX
+#define RK_RMAX 7
 #endif
+#ifndef RK_UNROLL
+#define RK_UNROLL 1
+#endif
+constexpr int kStepUnroll = RK_UNROLL;
 constexpr int kThreads = RK_THREADS;      // 8 warps per CTA
 constexpr int kMinBlocks = RK_MINBLOCKS;  // 2 CTAs / SM  -> <= 128 registers
 constexpr int kChunkKernels = 4;   // kernels per chunk (2 FFMA2 pairs)
@@ -40,8 +44,9 @@ constexpr unsigned kFull = 0xffffffffu;
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
 //           2: >= 3 channels (generic); 3: 1 channel, 1 pair
 constexpr int kNumR = 4;
-// positions per lane of class r_idx: 1,3,5,7 (RK_RSTEP 2) or 1,4,7,10 (3)
-__host__ __device__ constexpr int r_of(int r_idx) { return RK_RSTEP * r_idx + 1; }
+// positions per lane of class r_idx: 1, 3, 5, RK_RMAX (odd: spreads lanes
+// over the shared-memory banks)
+__host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 3 ? RK_RMAX : 2 * r_idx + 1; }
 constexpr int kNumNck = 4;
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
@@ -164,24 +169,34 @@ __device__ __forceinline__ void count_gt_live(unsigned& cnt, float a, float thr,
       : "f"(a), "f"(thr), "r"((unsigned)live));
 }
 
+// -(a > t) as an integer mask (set.gt.u32: 0xffffffff or 0) — ALU pipe.
+__device__ __forceinline__ unsigned gt_mask(float a, float t) {
+  unsigned m;
+  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(a), "f"(t));
+  return m;
+}
+
+// Unmasked pooling of R positions: per kernel, masks of two positions are
+// subtracted with one three-input add (FSET x2 + IADD3 per 2 outputs).
 template <int R, int P, bool MASKED>
 __device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R], const float (&thr)[2 * P],
                                             bool live) {
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
+  for (int p = 0; p < P; ++p) {
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const float a0 = acc[p][r].x, a1 = acc[p][r].y;
-      if (MASKED) {
-        count_gt_live(st.cnt[2 * p], a0, thr[2 * p], live);
-        count_gt_live(st.cnt[2 * p + 1], a1, thr[2 * p + 1], live);
-        st.mx[2 * p] = live ? fmaxf(st.mx[2 * p], a0) : st.mx[2 * p];
-        st.mx[2 * p + 1] = live ? fmaxf(st.mx[2 * p + 1], a1) : st.mx[2 * p + 1];
-      } else {
-        count_gt(st.cnt[2 * p], a0, thr[2 * p]);
-        count_gt(st.cnt[2 * p + 1], a1, thr[2 * p + 1]);
-        st.mx[2 * p] = fmaxf(st.mx[2 * p], a0);
-        st.mx[2 * p + 1] = fmaxf(st.mx[2 * p + 1], a1);
+    for (int h = 0; h < 2; ++h) {
+      const int g = 2 * p + h;
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        const float a0 = h ? acc[p][r].y : acc[p][r].x;
+        if (r + 1 < R) {
+          const float a1 = h ? acc[p][r + 1].y : acc[p][r + 1].x;
+          st.cnt[g] = st.cnt[g] - gt_mask(a0, thr[g]) - gt_mask(a1, thr[g]);
+          st.mx[g] = fmaxf(st.mx[g], fmaxf(a0, a1));
+        } else {
+          st.cnt[g] = st.cnt[g] - gt_mask(a0, thr[g]);
+          st.mx[g] = fmaxf(st.mx[g], a0);
+        }
       }
     }
   }
@@ -294,6 +309,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     int s = lane - a * d;
     int v0 = a * RD + s;
     const int dv = q32 * RD + r32;
+#pragma unroll(kStepUnroll)
     for (int stp = 0; stp < nfull; ++stp) {
       chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, one2, lo + v0, d, n, 0, 0, true);
       s += r32;
@@ -382,7 +398,7 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
         accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
       }
     }
-    pool_update<1, 1, true>(st, acc, thr, live);
+    pool_update_masked<1, 1>(st, acc, thr, live, 1, 1);
   }
   finish_chunk<2, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
