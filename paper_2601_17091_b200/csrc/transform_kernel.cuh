@@ -32,7 +32,7 @@ namespace rk {
 #define RK_RMAX 7
 #endif
 #ifndef RK_UNROLL
-#define RK_UNROLL 1
+#define RK_UNROLL 2
 #endif
 constexpr int kStepUnroll = RK_UNROLL;
 constexpr int kThreads = RK_THREADS;      // 8 warps per CTA
