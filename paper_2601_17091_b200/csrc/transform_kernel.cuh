@@ -1,4 +1,4 @@
-// transform_kernel.cuh — the sm_100a ROCKET transform kernel.
+// transform_kernel.cuh — the sm_100a ROCKET transform kernels.
 //
 // Replaces the numba hot loop _run_batch (reference:
 // /root/reference/pkg/src/gridrocket/engine.py:148-190).  For every
@@ -7,15 +7,33 @@
 // materialising the convolution output.
 //
 // Work decomposition:
-//   * CTA  = one staged series (all channels + zero halos in shared memory)
-//            and a block of "chunks" of the device bank;
-//   * warp = one chunk: up to 4 kernels (2 FFMA2 pairs) sharing
-//            (length, dilation, padding, channel set);
-//   * lane = R output positions u, u+d, ..., u+(R-1)d (stride = dilation),
-//            so one register window of R+LEN-1 series values feeds
-//            R*LEN taps of every kernel in the chunk.
-// Kernel pairs are packed into FFMA2 (sm_100 packed FP32) with the series
-// value as the scalar-broadcast operand.
+//   * chunk = up to 4 kernels (2 FFMA2 pairs) sharing (dilation, centre
+//             range [lo, lo+n), channel set) — one warp work unit;
+//   * lane  = R output positions u, u+d, ..., u+(R-1)d (stride = dilation),
+//             so one register window of R+LEN-1 series values feeds
+//             R*LEN taps of every kernel of the chunk;
+//   * kernel pairs are packed into FFMA2 (sm_100 packed FP32) with the
+//     series value as the scalar-broadcast operand.
+// Two kernels drive it:
+//   * rocket_warp_kernel  (series that fit 24 one-warp CTAs per SM): chunk
+//     descriptors and weights travel in the __grid_constant__ parameter
+//     block, so the weights sit in uniform registers (FFMA2 UR operands);
+//   * rocket_class_kernel (long / many-channel series): 8-warp CTAs share
+//     one staged series, weights come from global memory.
+//
+// Arithmetic (both modes are deterministic run to run):
+//   EXACT: acc = RN(acc + RN(w*x)) tap by tap from the first product
+//          (FMUL2, then FFMA2 with an opaque 1.0 so ptxas cannot contract
+//          the pair), channels then taps ascending, zero halos add +-0
+//          (never changes the sum).  Pooling compares acc > -bias
+//          (RN(acc + b) > 0 <=> acc > -b exactly) and the max is
+//          RN(max_t acc_t + b) == max_t RN(acc_t + b) — bit-identical to
+//          the reference (reference.py:1-17, engine.py:172-188).
+//   FAST:  the series is staged negated and the accumulator starts at -b,
+//          so acc' = -(b + sum w*x) via FFMA2 only.  "output > 0" is then
+//          the sign bit of acc' (acc' is never -0: its init is never -0
+//          and RN sums of non-(-0) terms are +0 when exactly zero), counted
+//          with one shift-add, and MAX = -min(acc').
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -34,10 +52,9 @@ namespace rk {
 #ifndef RK_UNROLL
 #define RK_UNROLL 2
 #endif
-constexpr int kStepUnroll = RK_UNROLL;
-constexpr int kThreads = RK_THREADS;      // 8 warps per CTA
-constexpr int kMinBlocks = RK_MINBLOCKS;  // 2 CTAs / SM  -> <= 128 registers
-constexpr int kChunkKernels = 4;   // kernels per chunk (2 FFMA2 pairs)
+constexpr int kStepUnroll = RK_UNROLL;    // full-step loop unroll
+constexpr int kThreads = RK_THREADS;      // class kernel: 8 warps per CTA
+constexpr int kMinBlocks = RK_MINBLOCKS;  // class kernel: 2 CTAs / SM
 constexpr unsigned kFull = 0xffffffffu;
 
 // Class encoding: cls = ((len_idx * kNumR) + r_idx) * kNumNck + nc_kind
@@ -50,11 +67,9 @@ __host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 3 ? RK_RMAX 
 constexpr int kNumNck = 4;
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
-// One warp work unit.  All kernels of a chunk have the same length,
-// dilation, padding and channel set, hence the same valid centre-position
-// range [lo, lo + n) (n == l_out, engine.py:163).
+// One chunk (class-kernel layout, global memory).
 struct __align__(16) DevChunk {
-  int len;    // taps: 7, 9 or 11
+  int len;    // taps: 7, 9 or 11 (shorter kernels zero-padded inside)
   int d;      // dilation
   int lo;     // first centre position u = t - p + c*d at t = 0
   int n;      // l_out
@@ -65,8 +80,8 @@ struct __align__(16) DevChunk {
   int chofs;  // offset into the channel-slot table (smem offsets)
   int pad_[3];
   int col[4];     // bank index of each kernel slot
-  float thr[4];   // count threshold: -bias (+0.0f, never -0)
-  float bias[4];  // added to the pooled max at the end (both modes)
+  float thr[4];   // exact: count threshold -bias (+0.0f, never -0)
+  float bias[4];  // bias (+0.0f: never -0)
 };
 static_assert(sizeof(DevChunk) == 96, "DevChunk layout");
 
@@ -81,7 +96,7 @@ struct LaunchArgs {
   const int* chan_off;     // device, per chunk slot: smem float offset of channel
   const int* block_start;  // device, n_blocks + 1 chunk boundaries (this class)
   unsigned long long* executed;  // device counter
-  int* item_counter;      // dynamic item scheduler (zeroed before the launch)
+  int* item_counter;       // dynamic item scheduler (zeroed before the launch)
   int n_blocks;
   int series_per_item;     // series staged together (small classes)
   int n_channels;
@@ -97,24 +112,22 @@ struct LaunchArgs {
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
-__device__ __forceinline__ float warp_max(float v) {
-  // order-preserving int mapping, then one REDUX.MAX
-  int i = __float_as_int(v);
-  int key = i >= 0 ? i : (i ^ 0x7fffffff);
-  key = __reduce_max_sync(kFull, key);
-  int back = key >= 0 ? key : (key ^ 0x7fffffff);
-  return __int_as_float(back);
+// order-preserving int key of a float (no NaNs here), for REDUX min/max
+__device__ __forceinline__ int fkey(float v) {
+  const int i = __float_as_int(v);
+  return i >= 0 ? i : (i ^ 0x7fffffff);
 }
+__device__ __forceinline__ float fkey_inv(int k) { return __int_as_float(k >= 0 ? k : (k ^ 0x7fffffff)); }
+__device__ __forceinline__ float warp_max(float v) { return fkey_inv(__reduce_max_sync(kFull, fkey(v))); }
+__device__ __forceinline__ float warp_min(float v) { return fkey_inv(__reduce_min_sync(kFull, fkey(v))); }
 
 // Accumulate one channel slot of a window into acc for P kernel pairs.
-// EXACT: acc = RN(acc + RN(w*x)) per tap (FMUL2, then FFMA2 with an opaque
-// 1.0 so the product is rounded on its own; reference.py:7-16).  FAST: one
-// FFMA2 per tap pair.  Both start from the first product (no bias in the
-// accumulator: the pooling compares against -bias and adds the bias to the
-// max at the end, RN(acc + b) > 0 <=> acc > -b).
+// FIRST && j == 0 starts the accumulator: EXACT from the first product,
+// FAST from init (-bias pair) with the first FFMA2.
 template <int LEN, int R, int P, bool EXACT, bool FIRST>
 __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w)[P][LEN],
-                                           const float (&xw)[R + LEN - 1], float2 one2) {
+                                           const float (&xw)[R + LEN - 1], const float2 (&init)[P],
+                                           float2 one2) {
 #pragma unroll
   for (int j = 0; j < LEN; ++j) {
 #pragma unroll
@@ -122,12 +135,13 @@ __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const float2 xv = make_float2(xw[r + j], xw[r + j]);
-        if (FIRST && j == 0) {
-          acc[p][r] = fmul2(w[p][j], xv);  // first tap: RN(w*x) == RN(+0 + RN(w*x))
-        } else if (EXACT) {
-          acc[p][r] = ffma2(fmul2(w[p][j], xv), one2, acc[p][r]);
+        if (EXACT) {
+          if (FIRST && j == 0)
+            acc[p][r] = fmul2(w[p][j], xv);  // RN(w*x) == RN(+0 + RN(w*x))
+          else
+            acc[p][r] = ffma2(fmul2(w[p][j], xv), one2, acc[p][r]);
         } else {
-          acc[p][r] = ffma2(w[p][j], xv, acc[p][r]);
+          acc[p][r] = ffma2(w[p][j], xv, (FIRST && j == 0) ? init[p] : acc[p][r]);
         }
       }
     }
@@ -151,92 +165,85 @@ __device__ __forceinline__ void load_window_clamped(float (&xw)[R + LEN - 1], co
   for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(max(u0 + (q - C) * d, lo_clamp), hi_clamp)];
 }
 
-// Per-lane pooled state for the kernels of one chunk.
+// Per-lane pooled state for the kernels of one chunk.  ext is the running
+// max (EXACT) or the running min of acc' = -(output) (FAST).
 template <int G>
 struct Pool {
   unsigned cnt[G];
-  float mx[G];
+  float ext[G];
 };
 
-// count += (a > thr): FSETP + predicated IADD, both on the ALU pipe (the
-// compiler's own select lowering puts an IMAD.MOV on the FMA pipe).
-__device__ __forceinline__ void count_gt(unsigned& cnt, float a, float thr) {
-  asm("{\n\t.reg .pred p;\n\tsetp.gt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(cnt) : "f"(a), "f"(thr));
+template <int G, bool EXACT>
+__device__ __forceinline__ void pool_init(Pool<G>& st) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    st.cnt[g] = 0u;
+    st.ext[g] = EXACT ? -INFINITY : INFINITY;
+  }
 }
-__device__ __forceinline__ void count_gt_live(unsigned& cnt, float a, float thr, bool live) {
+
+// count += (a > t): FSETP + predicated add, both on the ALU pipe.
+__device__ __forceinline__ void count_gt(unsigned& cnt, float a, float t, bool live) {
   asm("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %3, 0;\n\tsetp.gt.and.f32 p, %1, %2, q;\n\t@p add.u32 %0, %0, 1;\n\t}"
       : "+r"(cnt)
-      : "f"(a), "f"(thr), "r"((unsigned)live));
+      : "f"(a), "f"(t), "r"((unsigned)live));
 }
 
-// -(a > t) as an integer mask (set.gt.u32: 0xffffffff or 0) — ALU pipe.
-__device__ __forceinline__ unsigned gt_mask(float a, float t) {
-  unsigned m;
-  asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(a), "f"(t));
-  return m;
-}
-
-// Unmasked pooling of R positions: per kernel, masks of two positions are
-// subtracted with one three-input add (FSET x2 + IADD3 per 2 outputs).
-template <int R, int P, bool MASKED>
-__device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R], const float (&thr)[2 * P],
-                                            bool live) {
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int g = 2 * p + h;
-#pragma unroll
-      for (int r = 0; r < R; r += 2) {
-        const float a0 = h ? acc[p][r].y : acc[p][r].x;
-        if (r + 1 < R) {
-          const float a1 = h ? acc[p][r + 1].y : acc[p][r + 1].x;
-          st.cnt[g] = st.cnt[g] - gt_mask(a0, thr[g]) - gt_mask(a1, thr[g]);
-          st.mx[g] = fmaxf(st.mx[g], fmaxf(a0, a1));
-        } else {
-          st.cnt[g] = st.cnt[g] - gt_mask(a0, thr[g]);
-          st.mx[g] = fmaxf(st.mx[g], a0);
-        }
-      }
+// Pool one output of kernel slot g.
+template <bool EXACT, bool MASKED>
+__device__ __forceinline__ void pool_one(unsigned& cnt, float& ext, float a, float thr, bool ok) {
+  if (EXACT) {
+    if (MASKED) {
+      count_gt(cnt, a, thr, ok);
+      ext = ok ? fmaxf(ext, a) : ext;
+    } else {
+      count_gt(cnt, a, thr, true);
+      ext = fmaxf(ext, a);
+    }
+  } else {
+    // acc' < 0 <=> output > 0; acc' is never -0, so the sign bit decides
+    if (MASKED) {
+      if (ok) cnt += __float_as_uint(a) >> 31;
+      ext = ok ? fminf(ext, a) : ext;
+    } else {
+      cnt += __float_as_uint(a) >> 31;
+      ext = fminf(ext, a);
     }
   }
 }
 
-// Masked variant: position r of this lane is valid while r*d < nleft.
-template <int R, int P>
-__device__ __forceinline__ void pool_update_masked(Pool<2 * P>& st, const float2 (&acc)[P][R],
-                                                   const float (&thr)[2 * P], bool live, int nleft, int d) {
+// Pool R positions of P kernel pairs; position r is valid while
+// r*d < nleft (MASKED only).
+template <int R, int P, bool EXACT, bool MASKED>
+__device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R], const float (&thr)[2 * P],
+                                            bool live, int nleft, int d) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const bool ok = live && (r * d < nleft);
+    const bool ok = !MASKED || (live && (r * d < nleft));
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      const float a0 = acc[p][r].x, a1 = acc[p][r].y;
-      count_gt_live(st.cnt[2 * p], a0, thr[2 * p], ok);
-      count_gt_live(st.cnt[2 * p + 1], a1, thr[2 * p + 1], ok);
-      st.mx[2 * p] = ok ? fmaxf(st.mx[2 * p], a0) : st.mx[2 * p];
-      st.mx[2 * p + 1] = ok ? fmaxf(st.mx[2 * p + 1], a1) : st.mx[2 * p + 1];
+      pool_one<EXACT, MASKED>(st.cnt[2 * p], st.ext[2 * p], acc[p][r].x, thr[2 * p], ok);
+      pool_one<EXACT, MASKED>(st.cnt[2 * p + 1], st.ext[2 * p + 1], acc[p][r].y, thr[2 * p + 1], ok);
     }
   }
 }
 
-// Finish one chunk: reduce the per-lane pools over the warp and store
-// out[row, col*fpk] = ppv, out[row, col*fpk + 1] = max (engine.py:186-188).
+// Finish one chunk: reduce the per-lane pools over the warp; lane g
+// finishes kernel g: out[row, col*fpk] = ppv, out[row, col*fpk+1] = max
+// (engine.py:186-188).
 template <int G, bool EXACT, class CH>
 __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __restrict__ orow, int fpk,
                                              int vec_out, int lane) {
-  // reduce every kernel over the warp, then lane g finishes kernel g (one
-  // float64 division per lane in parallel instead of G divergent ones)
   unsigned my_cnt = 0;
-  float my_max = -INFINITY, my_bias = 0.0f;
+  float my_ext = 0.0f, my_bias = 0.0f;
   int my_col = 0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const unsigned tot = __reduce_add_sync(kFull, st.cnt[g]);
-    const float m = warp_max(st.mx[g]);
+    const float e = EXACT ? warp_max(st.ext[g]) : warp_min(st.ext[g]);
     if (lane == g) {
       my_cnt = tot;
-      my_max = m;
+      my_ext = e;
       my_bias = c.bias[g];
       my_col = c.col[g];
     }
@@ -244,8 +251,8 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
   if (lane < c.nk) {
     // ppv: count / l_out divided in float64, stored as float32 (engine.py:187)
     const float ppv = __double2float_rn(__ddiv_rn((double)my_cnt, (double)c.n));
-    // max: RN(max_t acc_t + b) == max_t RN(acc_t + b) (RN(. + b) is monotone)
-    const float mx = __fadd_rn(my_max, my_bias);
+    // exact: RN(max_t acc_t + b) == max_t RN(acc_t + b); fast: -min acc'
+    const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
     float* dst = orow + (int64_t)my_col * fpk;
     if (vec_out) {
       *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
@@ -257,12 +264,11 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
 }
 
 // One step: R positions per lane (u0, u0+d, ..., u0+(R-1)d) for P kernel
-// pairs over NC channel slots.  Weights are register-resident (NC*P*LEN
-// float2) or, for the generic channel count, re-read per slot.
+// pairs over NC channel slots.
 template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                           float2 one2, int u0, int d, int nleft,
+                                           const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
                                            int lo_clamp, int hi_clamp, bool live) {
   float2 acc[P][R];
 #pragma unroll
@@ -272,16 +278,12 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
       load_window_clamped<LEN, R>(xw, chan[s], u0, d, lo_clamp, hi_clamp);
     else
       load_window<LEN, R>(xw, chan[s], u0, d);
-    if (s == 0) {
-      accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, one2);
-    } else {
-      accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, one2);
-    }
+    if (s == 0)
+      accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, init, one2);
+    else
+      accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, init, one2);
   }
-  if (MASKED)
-    pool_update_masked<R, P>(st, acc, thr, live, nleft, d);
-  else
-    pool_update<R, P, false>(st, acc, thr, true);
+  pool_update<R, P, EXACT, MASKED>(st, acc, thr, live, nleft, d);
 }
 
 // Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
@@ -289,12 +291,12 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
 // lanes in consecutive order (consecutive s -> consecutive smem addresses;
 // R odd spreads consecutive a over the banks).  Steps whose 32 starts are
 // all complete runs go through the unmasked path; the remaining starts
-// (incomplete 32-groups and the final partial run, whose positions
-// v0 + r*d may pass n) through one or two masked steps with clamped reads.
+// (an incomplete 32-group and the final partial run, whose positions
+// v0 + r*d may pass n) through masked steps with clamped reads.
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                              float2 one2, int lo, int n, int d,
+                                              const float2 (&init)[P], float2 one2, int lo, int n, int d,
                                               int lo_clamp, int hi_clamp, int lane) {
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
@@ -311,7 +313,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     const int dv = q32 * RD + r32;
 #pragma unroll(kStepUnroll)
     for (int stp = 0; stp < nfull; ++stp) {
-      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, one2, lo + v0, d, n, 0, 0, true);
+      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, 0, true);
       s += r32;
       v0 += dv;
       if (s >= d) {
@@ -326,12 +328,52 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
     const int ii = live ? i : 0;
     const int a = ii / d;
     const int v0 = a * RD + (ii - a * d);
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
                                           live);
   }
 }
 
-// One chunk, NC channel slots with register-resident weights.
+// Per-chunk constants of the pooling: exact thresholds, fast init pairs
+// (-bias, moved through a shuffle so they live in vector registers and the
+// first FFMA2 can read them next to a uniform-register weight).
+template <int P, bool EXACT, class CH>
+__device__ __forceinline__ void chunk_consts(const CH& c, float (&thr)[2 * P], float2 (&init)[P]) {
+#pragma unroll
+  for (int g = 0; g < 2 * P; ++g) thr[g] = EXACT ? c.thr[g] : 0.0f;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    if (EXACT) {
+      init[p] = make_float2(0.0f, 0.0f);
+    } else {
+      init[p].x = __shfl_sync(kFull, -c.bias[2 * p] + 0.0f, 0);
+      init[p].y = __shfl_sync(kFull, -c.bias[2 * p + 1] + 0.0f, 0);
+    }
+  }
+}
+
+// Stage series rows [xs, xs + rows*L) into smem rows of stride S at offset
+// H (negated for FAST).
+template <bool EXACT>
+__device__ __forceinline__ void stage_rows(float* __restrict__ smem, const float* __restrict__ xs, int rows, int L,
+                                           int S, int H, int vec_in, int tid, int nthreads) {
+  const float sg = EXACT ? 1.0f : -1.0f;
+  if (vec_in) {
+    const int L4 = L >> 2;
+    for (int k = tid; k < rows * L4; k += nthreads) {
+      const int row = k / L4, t = k - row * L4;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)row * L) + t);
+      *reinterpret_cast<float4*>(smem + row * S + H + 4 * t) = make_float4(sg * v.x, sg * v.y, sg * v.z, sg * v.w);
+    }
+  } else {
+    for (int k = tid; k < rows * L; k += nthreads) {
+      const int row = k / L, t = k - row * L;
+      smem[row * S + H + t] = sg * __ldg(xs + k);
+    }
+  }
+}
+
+// One chunk with NC channel slots and register-resident weights (class
+// kernel).
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __restrict__ sx,
                                           const float* __restrict__ weights, const int* __restrict__ chan_off,
@@ -350,34 +392,31 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
 #pragma unroll
   for (int s = 0; s < NC; ++s) chan[s] = sx + __ldg(chan_off + c.chofs + s);
   float thr[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) thr[g] = c.thr[g];
+  float2 init[P];
+  chunk_consts<P, EXACT>(c, thr, init);
   Pool<G> st;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    st.cnt[g] = 0u;
-    st.mx[g] = -INFINITY;
-  }
-  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, make_float2(one, one), c.lo, c.n, c.d, -halo,
+  pool_init<G, EXACT>(st);
+  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, -halo,
                                       L + halo - 1, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
-// Generic channel count (>= 3 slots): one kernel pair, slots looped at run
-// time; the pooled accumulator continues across slots in slot order.
-template <int LEN, int R, bool EXACT>
+// Generic channel count (>= 3 slots): one kernel pair, one position per
+// lane, slots looped at run time (the accumulator continues across slots in
+// slot order, as the reference's channel loop).
+template <int LEN, bool EXACT>
 __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float* __restrict__ sx,
                                                   const float* __restrict__ weights,
                                                   const int* __restrict__ chan_off, float* __restrict__ orow,
                                                   int fpk, int vec_out, float one, int lane) {
-  // Positions one per lane (R = 1 semantics), window re-read per slot.
   constexpr int C = (LEN - 1) / 2;
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
-  float thr[2] = {c.thr[0], c.thr[1]};
+  float thr[2];
+  float2 init[1];
+  chunk_consts<1, EXACT>(c, thr, init);
   const float2 one2 = make_float2(one, one);
   Pool<2> st;
-  st.cnt[0] = st.cnt[1] = 0u;
-  st.mx[0] = st.mx[1] = -INFINITY;
+  pool_init<2, EXACT>(st);
   const int d = c.d, n = c.n, lo = c.lo, nc = c.nc;
   for (int t0 = 0; t0 < n; t0 += 32) {
     const int t = t0 + lane;
@@ -392,21 +431,21 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
       float2 w[1][LEN];
 #pragma unroll
       for (int j = 0; j < LEN; ++j) w[0][j] = __ldg(wp + s * LEN + j);
-      if (s == 0) {
-        accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, one2);
-      } else {
-        accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, one2);
-      }
+      if (s == 0)
+        accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, init, one2);
+      else
+        accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, init, one2);
     }
-    pool_update_masked<1, 1>(st, acc, thr, live, 1, 1);
+    pool_update<1, 1, EXACT, true>(st, acc, thr, live, 1, 1);
   }
   finish_chunk<2, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
-// One launch per chunk class <LEN, R, NCK>: each class gets its own
-// register allocation and straight-line code (no dispatch in the warp loop).
-// Items are (series, block of this class's chunks); a CTA stages the series
-// once per item and its warps pull chunks with a shared-memory counter.
+// ---------------------------------------------------------------------------
+// Class kernel: one launch per chunk class <LEN, R, NCK>.  Items are
+// (group of series, block of this class's chunks); a CTA stages the series
+// once per item and its warps pull chunks with a shared-memory counter;
+// items are claimed dynamically.
 template <int LEN, int R, int NCK, bool EXACT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(const LaunchArgs a) {
   extern __shared__ __align__(16) float smem[];
@@ -423,8 +462,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
     if (t < H || t >= H + L) smem[k] = 0.0f;
   }
   unsigned long long done = 0;
-  // Items are claimed dynamically: CTAs of this launch that start late
-  // (while the previous class's tail still occupies SMs) simply take fewer.
   while (true) {
     __syncthreads();  // every warp has left the previous item
     if (tid == 0) s_item = atomicAdd(a.item_counter, 1);
@@ -436,21 +473,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
     const int64_t series0 = group * SPI;
     const int64_t left = a.n_series - series0;
     const int ns = left < SPI ? (int)left : SPI;
-    const float* xs = a.x + series0 * (int64_t)C * L;
-    if (a.vec_in) {
-      const int L4 = L >> 2;
-      for (int k = tid; k < ns * C * L4; k += kThreads) {
-        const int row = k / L4, t = k - row * L4;  // row = series * C + channel
-        const float4 v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)row * L) + t);
-        float* dst = smem + row * S + H + 4 * t;
-        dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
-      }
-    } else {
-      for (int k = tid; k < ns * C * L; k += kThreads) {
-        const int row = k / L, t = k - row * L;
-        smem[row * S + H + t] = __ldg(xs + k);
-      }
-    }
+    stage_rows<EXACT>(smem, a.x + series0 * (int64_t)C * L, ns * C, L, S, H, a.vec_in, tid, kThreads);
     if (tid == 0) s_next = 0;
     __syncthreads();
     const int cbeg = __ldg(a.block_start + blk);
@@ -473,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
       else if (NCK == 3)
         run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
       else
-        run_chunk_generic<LEN, R, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
+        run_chunk_generic<LEN, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
     }
   }
@@ -485,14 +508,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
 // descriptors and weights of one launch travel in the kernel's
 // __grid_constant__ parameter block (<= 32 KB); the chunk loop counter is
 // warp-uniform, so ptxas keeps the weights in uniform registers (LDCU) and
-// FFMA2 reads them as UR operands — ~60 vector registers instead of ~120,
+// FFMA2 reads them as UR operands — ~70 vector registers instead of ~120,
 // hence 1.5x the resident warps of the class kernel.  Each CTA stages its
 // own copy of the series (C * sstride floats) and claims series dynamically.
 constexpr int kWarpCtasPerSm = 24;
+constexpr int kParamBytes = 32000;
 struct float4_t {  // host-side storage of the parameter blob
   float x, y, z, w;
 };
-constexpr int kParamBytes = 32000;
 
 struct __align__(16) WChunk {  // 80 bytes
   int d, lo, n, nk;
@@ -551,20 +574,7 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
     item = __shfl_sync(kFull, item, 0);
     if (item >= p.h.n_series) break;
     __syncwarp();
-    const float* xs = p.h.x + (int64_t)item * C * L;
-    if (p.h.vec_in) {
-      const int L4 = L >> 2;
-      for (int k = lane; k < C * L4; k += 32) {
-        const int ch = k / L4, t = k - ch * L4;
-        const float4 v = __ldg(reinterpret_cast<const float4*>(xs + (int64_t)ch * L) + t);
-        *reinterpret_cast<float4*>(smem + ch * S + H + 4 * t) = v;
-      }
-    } else {
-      for (int k = lane; k < C * L; k += 32) {
-        const int ch = k / L, t = k - ch * L;
-        smem[ch * S + H + t] = __ldg(xs + k);
-      }
-    }
+    stage_rows<EXACT>(smem, p.h.x + (int64_t)item * C * L, C, L, S, H, p.h.vec_in, lane, 32);
     __syncwarp();
     float* orow = p.h.out + (int64_t)item * p.h.ld_out;
     for (int ci = 0; ci < p.h.n_chunks; ++ci) {
@@ -581,15 +591,11 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
 #pragma unroll
       for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
       float thr[2 * P];
-#pragma unroll
-      for (int g = 0; g < 2 * P; ++g) thr[g] = c.thr[g];
+      float2 init[P];
+      chunk_consts<P, EXACT>(c, thr, init);
       Pool<2 * P> st;
-#pragma unroll
-      for (int g = 0; g < 2 * P; ++g) {
-        st.cnt[g] = 0u;
-        st.mx[g] = -INFINITY;
-      }
-      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
+      pool_init<2 * P, EXACT>(st);
+      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
       finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
     }
