@@ -1,0 +1,55 @@
+"""The C ABI library loads and exports every symbol include/*.h declares
+(no compute calls: this container has no GPU)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2601_17091_b200 import _lib
+
+HEADER = os.path.join(_lib.INCLUDE, "rocket_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rk_\w+)\s*\(", text)))
+
+
+def test_header_declares_expected_entry_points():
+    syms = declared_symbols()
+    assert set(syms) == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.fail(f"{_lib.LIB_PATH} not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing
+
+
+def test_abi_version_and_device_count_without_gpu():
+    lib = _lib.load()
+    assert lib.rk_abi_version() == 1
+    n = _lib.device_count()
+    assert n >= 0
+
+
+def test_bank_create_reports_errors_not_crashes():
+    """Argument validation happens before any device work."""
+    lib = _lib.load()
+    handle = ctypes.c_void_p()
+    rc = lib.rk_bank_create(0, 1, 64, None, None, None, None, None, None, None, None, None, 0,
+                            ctypes.byref(handle))
+    assert rc == _lib.RK_ERR_INVALID
+    assert "at least one kernel" in _lib.last_error()
+
+
+def test_run_batch_rejects_bad_workers():
+    lib = _lib.load()
+    rc = lib.rk_run_batch_f32(None, 0, 1, 64, None, None, None, None, None, None, None, None, None, 1, 0, 2, None,
+                              2, 0)
+    assert rc == -_lib.RK_ERR_INVALID
