@@ -158,12 +158,17 @@ namespace {
 // Host-buffer transforms run on a pooled "worker": two streams, two events
 // and double-buffered device scratch, reused across calls (per-call
 // allocation made the stream-ordered pool map and unmap memory every call).
+// Pipeline: h2d stream -> compute stream -> d2h stream, 3 input and 2
+// output buffers; H2D of batch k+1 is enqueued before the D2H of batch k so
+// a copy engine never holds the next input behind a long feature copy.
+constexpr int kInBufs = 3, kOutBufs = 2;
 struct Worker {
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t in_ready[kInBufs] = {}, in_free[kInBufs] = {};
+  cudaEvent_t out_ready[kOutBufs] = {}, out_free[kOutBufs] = {};
   unsigned long long* d_scratch = nullptr;
-  float* d_in[2] = {nullptr, nullptr};
-  float* d_out[2] = {nullptr, nullptr};
+  float* d_in[kInBufs] = {};
+  float* d_out[kOutBufs] = {};
   size_t in_cap = 0, out_cap = 0;
 };
 
@@ -265,8 +270,16 @@ int acquire_worker(DeviceState* st, Worker** out) {
   }
   Worker* w = new Worker();
   RK_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
-  RK_CUDA(cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) RK_CUDA(cudaEventCreateWithFlags(&w->ev[i], cudaEventDisableTiming));
+  RK_CUDA(cudaStreamCreateWithFlags(&w->h2d_stream, cudaStreamNonBlocking));
+  RK_CUDA(cudaStreamCreateWithFlags(&w->d2h_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < kInBufs; ++i) {
+    RK_CUDA(cudaEventCreateWithFlags(&w->in_ready[i], cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&w->in_free[i], cudaEventDisableTiming));
+  }
+  for (int i = 0; i < kOutBufs; ++i) {
+    RK_CUDA(cudaEventCreateWithFlags(&w->out_ready[i], cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&w->out_free[i], cudaEventDisableTiming));
+  }
   RK_CUDA(cudaMalloc(&w->d_scratch, kScratchBytes));
   *out = w;
   return RK_OK;
@@ -843,9 +856,8 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     }
     return RK_OK;
   }
-  // Host buffers: row batches through a pooled worker's device buffers,
-  // double-buffered so batch i+1's H2D and batch i-1's D2H overlap batch
-  // i's kernels.
+  // Host buffers: row batches through a pooled worker's device buffers on
+  // three streams (see Worker).
   Worker* w = nullptr;
   rc = acquire_worker(st, &w);
   if (rc) return rc;
@@ -854,18 +866,18 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     Worker* w;
     ~Release() { release_worker(st, w); }
   } release{st, w};
-  cudaStream_t stream = w->stream, copy_stream = w->copy_stream;
+  cudaStream_t stream = w->stream;
   const int64_t out_row_bytes = b->K * fpk * 4;
   const int64_t in_row_bytes = row_in * 4;
-  const int64_t budget = (int64_t)1 << 30;  // device scratch per buffer
-  int64_t batch = std::max<int64_t>(1, budget / (out_row_bytes + in_row_bytes));
+  const int64_t budget = (int64_t)1 << 30;  // device scratch per output buffer
+  int64_t batch = std::max<int64_t>(1, budget / out_row_bytes);
   batch = std::min<int64_t>(batch, n);
-  // at least four batches when there is enough work to overlap copies
-  if (n >= 4096) batch = std::min<int64_t>(batch, (n + 3) / 4);
+  // several batches when there is enough work to overlap the copies
+  if (n >= 4096) batch = std::min<int64_t>(batch, (n + 5) / 6);
   if (!dx) {
     const size_t need = (size_t)(batch * in_row_bytes);
     if (need > w->in_cap) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kInBufs; ++i) {
         if (w->d_in[i]) RK_CUDA(cudaFree(w->d_in[i]));
         w->d_in[i] = nullptr;
         RK_CUDA(cudaMalloc(&w->d_in[i], need));
@@ -876,7 +888,7 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
   if (!dout) {
     const size_t need = (size_t)(batch * out_row_bytes);
     if (need > w->out_cap) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kOutBufs; ++i) {
         if (w->d_out[i]) RK_CUDA(cudaFree(w->d_out[i]));
         w->d_out[i] = nullptr;
         RK_CUDA(cudaMalloc(&w->d_out[i], need));
@@ -886,38 +898,55 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
   }
   unsigned long long* d_exec = w->d_scratch;
   RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
-  int64_t bi = 0;
-  for (int64_t s0 = 0; s0 < n; s0 += batch, ++bi) {
-    const int64_t cnt = std::min(batch, n - s0);
-    const int k = (int)(bi & 1);
+  const int64_t nbatch = (n + batch - 1) / batch;
+  auto h2d = [&](int64_t k) -> int {
+    const int64_t s0 = k * batch, cnt = std::min(batch, n - s0);
+    const int ib = (int)(k % kInBufs);
+    if (k >= kInBufs) RK_CUDA(cudaStreamWaitEvent(w->h2d_stream, w->in_free[ib], 0));
+    RK_CUDA(cudaMemcpyAsync(w->d_in[ib], x + s0 * row_in, cnt * in_row_bytes, cudaMemcpyHostToDevice,
+                            w->h2d_stream));
+    RK_CUDA(cudaEventRecord(w->in_ready[ib], w->h2d_stream));
+    return RK_OK;
+  };
+  if (!dx) {
+    rc = h2d(0);
+    if (rc) return rc;
+  }
+  for (int64_t k = 0; k < nbatch; ++k) {
+    const int64_t s0 = k * batch, cnt = std::min(batch, n - s0);
+    const int ib = (int)(k % kInBufs), ob = (int)(k % kOutBufs);
+    if (!dx && k + 1 < nbatch) {
+      rc = h2d(k + 1);  // enqueued before this batch's D2H
+      if (rc) return rc;
+    }
     const float* kx = x + s0 * row_in;
     if (!dx) {
-      RK_CUDA(cudaMemcpyAsync(w->d_in[k], kx, cnt * in_row_bytes, cudaMemcpyHostToDevice, stream));
-      kx = w->d_in[k];
+      RK_CUDA(cudaStreamWaitEvent(stream, w->in_ready[ib], 0));
+      kx = w->d_in[ib];
     }
-    float* ko = dout ? out + (row0 + s0) * ld_out : w->d_out[k];
+    float* ko = dout ? out + (row0 + s0) * ld_out : w->d_out[ob];
     const int64_t kld = dout ? ld_out : b->K * fpk;
+    if (!dout && k >= kOutBufs) RK_CUDA(cudaStreamWaitEvent(stream, w->out_free[ob], 0));
     rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec, reinterpret_cast<int*>(d_exec + 1));
     if (rc) return rc;
+    if (!dx) RK_CUDA(cudaEventRecord(w->in_free[ib], stream));
     if (!dout) {
-      // D2H on the copy stream so the next batch's kernels can start.
-      RK_CUDA(cudaEventRecord(w->ev[k], stream));
-      RK_CUDA(cudaStreamWaitEvent(copy_stream, w->ev[k], 0));
+      RK_CUDA(cudaEventRecord(w->out_ready[ob], stream));
+      RK_CUDA(cudaStreamWaitEvent(w->d2h_stream, w->out_ready[ob], 0));
       float* hdst = out + (row0 + s0) * ld_out;
       if (ld_out == kld) {
-        RK_CUDA(cudaMemcpyAsync(hdst, w->d_out[k], cnt * out_row_bytes, cudaMemcpyDeviceToHost, copy_stream));
+        RK_CUDA(cudaMemcpyAsync(hdst, w->d_out[ob], cnt * out_row_bytes, cudaMemcpyDeviceToHost, w->d2h_stream));
       } else {
-        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, w->d_out[k], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
-                                  copy_stream));
+        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, w->d_out[ob], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
+                                  w->d2h_stream));
       }
-      // the next use of buffer k waits for this copy
-      RK_CUDA(cudaEventRecord(w->ev[k], copy_stream));
-      RK_CUDA(cudaStreamWaitEvent(stream, w->ev[k], 0));
+      RK_CUDA(cudaEventRecord(w->out_free[ob], w->d2h_stream));
     }
   }
   unsigned long long h = 0;
   RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));
-  RK_CUDA(cudaStreamSynchronize(copy_stream));
+  RK_CUDA(cudaStreamSynchronize(w->d2h_stream));
+  RK_CUDA(cudaStreamSynchronize(w->h2d_stream));
   RK_CUDA(cudaStreamSynchronize(stream));
   if (executed) *executed = (int64_t)h;
   return RK_OK;
@@ -1012,14 +1041,20 @@ int rk_release_caches(void) {
     cudaSetDevice(kv.first);
     std::lock_guard<std::mutex> pl(st->pool_mu);
     for (Worker* w : st->free_workers) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kInBufs; ++i) {
         cudaFree(w->d_in[i]);
+        cudaEventDestroy(w->in_ready[i]);
+        cudaEventDestroy(w->in_free[i]);
+      }
+      for (int i = 0; i < kOutBufs; ++i) {
         cudaFree(w->d_out[i]);
-        cudaEventDestroy(w->ev[i]);
+        cudaEventDestroy(w->out_ready[i]);
+        cudaEventDestroy(w->out_free[i]);
       }
       cudaFree(w->d_scratch);
       cudaStreamDestroy(w->stream);
-      cudaStreamDestroy(w->copy_stream);
+      cudaStreamDestroy(w->h2d_stream);
+      cudaStreamDestroy(w->d2h_stream);
       delete w;
     }
     st->free_workers.clear();
