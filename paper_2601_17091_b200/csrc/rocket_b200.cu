@@ -655,6 +655,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       dc.n = n;
       dc.nk = nk;
       dc.nc = nc;
+      dc.q32 = 32 / d;
+      dc.r32 = 32 % d;
+      dc.invd = 1.0f / (float)d;
       int best_r = 0;
       int64_t best = INT64_MAX;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
@@ -765,6 +768,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
               wc.thr[g] = c.thr[g];
             }
             for (int s2 = 0; s2 < NC; ++s2) wc.ch[s2] = chan_off[c.chofs + s2] / (int)sstride;
+            wc.q32 = (short)c.q32;
+            wc.r32 = (short)c.r32;
+            wc.invd = c.invd;
             std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
             std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
             wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;

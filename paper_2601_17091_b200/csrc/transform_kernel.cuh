@@ -78,7 +78,9 @@ struct __align__(16) DevChunk {
   int cls;    // dispatch class
   int wofs;   // float offset into the packed weights
   int chofs;  // offset into the channel-slot table (smem offsets)
-  int pad_[3];
+  int q32;    // 32 / d       (lane map, precomputed on the host)
+  int r32;    // 32 % d
+  float invd; // 1 / d        (lane / d for lane < 32 via one multiply)
   int col[4];     // bank index of each kernel slot
   float thr[4];   // exact: count threshold -bias (+0.0f, never -0)
   float bias[4];  // bias (+0.0f: never -0)
@@ -126,7 +128,7 @@ __device__ __forceinline__ float warp_min(float v) { return fkey_inv(__reduce_mi
 // FAST from init (-bias pair) with the first FFMA2.
 template <int LEN, int R, int P, bool EXACT, bool FIRST>
 __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w)[P][LEN],
-                                           const float (&xw)[R + LEN - 1], const float2 (&init)[P],
+                                           const float (&xw)[R + LEN - 1], const float2 (&init)[P][R],
                                            float2 one2) {
 #pragma unroll
   for (int j = 0; j < LEN; ++j) {
@@ -141,7 +143,7 @@ __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w
           else
             acc[p][r] = ffma2(fmul2(w[p][j], xv), one2, acc[p][r]);
         } else {
-          acc[p][r] = ffma2(w[p][j], xv, (FIRST && j == 0) ? init[p] : acc[p][r]);
+          acc[p][r] = ffma2(w[p][j], xv, (FIRST && j == 0) ? init[p][r] : acc[p][r]);
         }
       }
     }
@@ -157,12 +159,16 @@ __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const floa
   for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
 }
 
+// Masked steps: positions past n read past the staged row; only the upper
+// end needs a clamp (for a live lane u0 - C*d >= lo - C*d = -p_C >= -halo,
+// where p_C is the padding of the chunk's longest kernel).
 template <int LEN, int R>
 __device__ __forceinline__ void load_window_clamped(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
-                                                    int u0, int d, int lo_clamp, int hi_clamp) {
+                                                    int u0, int d, int hi_clamp) {
   constexpr int C = (LEN - 1) / 2;
+  const int i0 = u0 - C * d;
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(max(u0 + (q - C) * d, lo_clamp), hi_clamp)];
+  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(i0 + q * d, hi_clamp)];
 }
 
 // Per-lane pooled state for the kernels of one chunk.  ext is the running
@@ -269,21 +275,35 @@ template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                            const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
-                                           int lo_clamp, int hi_clamp, bool live) {
+                                           int hi_clamp, bool live) {
+  // FAST masked steps start dead positions at +inf: inf + finite stays
+  // +inf, which has a clear sign bit (not counted) and never lowers the min
+  float2 init_r[P][R];
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (MASKED && !EXACT) {
+        const bool ok = live && (r * d < nleft);
+        init_r[p][r] = ok ? init[p] : make_float2(INFINITY, INFINITY);
+      } else {
+        init_r[p][r] = init[p];
+      }
+    }
   float2 acc[P][R];
 #pragma unroll
   for (int s = 0; s < NC; ++s) {
     float xw[R + LEN - 1];
     if (MASKED)
-      load_window_clamped<LEN, R>(xw, chan[s], u0, d, lo_clamp, hi_clamp);
+      load_window_clamped<LEN, R>(xw, chan[s], u0, d, hi_clamp);
     else
       load_window<LEN, R>(xw, chan[s], u0, d);
     if (s == 0)
-      accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, init, one2);
+      accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, init_r, one2);
     else
-      accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, init, one2);
+      accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, init_r, one2);
   }
-  pool_update<R, P, EXACT, MASKED>(st, acc, thr, live, nleft, d);
+  pool_update<R, P, EXACT, MASKED && EXACT>(st, acc, thr, live, nleft, d);
 }
 
 // Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
@@ -296,40 +316,41 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                              const float2 (&init)[P], float2 one2, int lo, int n, int d,
-                                              int lo_clamp, int hi_clamp, int lane) {
+                                              const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
+                                              int r32, float invd, int hi_clamp, int lane) {
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
   const int full_starts = A * d;
   const int starts = full_starts + min(d, rem);
   const int nfull = full_starts >> 5;
-  if (nfull > 0) {
-    // incremental (a, s) = divmod(32*step + lane, d)
-    const int q32 = 32 / d, r32 = 32 - q32 * d;
-    int a = lane / d;
-    int s = lane - a * d;
-    int v0 = a * RD + s;
-    const int dv = q32 * RD + r32;
+  // (a, s) = divmod(32*step + lane, d), advanced incrementally; the first
+  // divmod of lane < 32 is exact in float ((lane + 0.5) / d is never within
+  // 2^-20 of an integer)
+  int a = (int)((lane + 0.5f) * invd);
+  int s = lane - a * d;
+  int v0 = a * RD + s;
+  const int dv = q32 * RD + r32;
 #pragma unroll(kStepUnroll)
-    for (int stp = 0; stp < nfull; ++stp) {
-      chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, 0, true);
-      s += r32;
-      v0 += dv;
-      if (s >= d) {
-        s -= d;
-        v0 += RD - d;
-      }
+  for (int stp = 0; stp < nfull; ++stp) {
+    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, true);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
     }
   }
   for (int base = nfull << 5; base < starts; base += 32) {
-    const int i = base + lane;
-    const bool live = i < starts;
-    const int ii = live ? i : 0;
-    const int a = ii / d;
-    const int v0 = a * RD + (ii - a * d);
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + v0, d, n - v0, lo_clamp, hi_clamp,
-                                          live);
+    const bool live = base + lane < starts;
+    const int vv = live ? v0 : 0;
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + vv, d, n - vv, hi_clamp, live);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
+    }
   }
 }
 
@@ -396,8 +417,8 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
   chunk_consts<P, EXACT>(c, thr, init);
   Pool<G> st;
   pool_init<G, EXACT>(st);
-  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, -halo,
-                                      L + halo - 1, lane);
+  run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, c.q32,
+                                      c.r32, c.invd, L + halo - 1, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
@@ -423,6 +444,7 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
     const bool live = t < n;
     const int u = lo + (live ? t : 0);
     float2 acc[1][1];
+    float2 init_r[1][1] = {{EXACT ? init[0] : (live ? init[0] : make_float2(INFINITY, INFINITY))}};
     for (int s = 0; s < nc; ++s) {
       const float* p = sx + __ldg(chan_off + c.chofs + s) + (u - C * d);
       float xw[LEN];
@@ -432,11 +454,11 @@ __device__ __forceinline__ void run_chunk_generic(const DevChunk& c, const float
 #pragma unroll
       for (int j = 0; j < LEN; ++j) w[0][j] = __ldg(wp + s * LEN + j);
       if (s == 0)
-        accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, init, one2);
+        accumulate<LEN, 1, 1, EXACT, true>(acc, w, xw, init_r, one2);
       else
-        accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, init, one2);
+        accumulate<LEN, 1, 1, EXACT, false>(acc, w, xw, init_r, one2);
     }
-    pool_update<1, 1, EXACT, true>(st, acc, thr, live, 1, 1);
+    pool_update<1, 1, EXACT, EXACT>(st, acc, thr, live, 1, 1);
   }
   finish_chunk<2, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
@@ -522,8 +544,10 @@ struct __align__(16) WChunk {  // 80 bytes
   int col[4];
   float bias[4];
   float thr[4];
-  int ch[2];  // channel slots (smem offsets are ch * sstride)
-  int pad_[2];
+  int ch[2];   // channel slots (smem offsets are ch * sstride)
+  short q32;   // 32 / d (lane map, precomputed on the host)
+  short r32;   // 32 % d
+  float invd;  // 1 / d
 };
 static_assert(sizeof(WChunk) == 80, "WChunk layout");
 
@@ -595,7 +619,8 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
       chunk_consts<P, EXACT>(c, thr, init);
       Pool<2 * P> st;
       pool_init<2 * P, EXACT>(st);
-      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, -H, L + H - 1, lane);
+      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
+                                          L + H - 1, lane);
       finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
     }
