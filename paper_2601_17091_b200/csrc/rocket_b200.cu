@@ -446,7 +446,11 @@ int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_o
     const int want = (4 * rk::kThreads / 32 + nchunks - 1) / nchunks;
     while (spi < want && spi < 16 && (int64_t)(spi + 1) * series_bytes <= smem_cap / 2 && spi < n) ++spi;
     const int smem = spi * series_bytes;
-    const int ctas_per_sm = 2 * smem + 2048 <= (int)st->smem_optin ? 2 : 1;
+    int rc0 = set_kernel_smem(st, fn, smem);
+    if (rc0) return rc0;
+    int ctas_per_sm = 1;
+    RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, (const void*)fn, rk::kThreads, smem));
+    ctas_per_sm = std::max(1, ctas_per_sm);
     const int64_t resident = (int64_t)st->sms * ctas_per_sm;
     const int64_t groups = (n + spi - 1) / spi;
     int nb = 1;

@@ -41,10 +41,10 @@
 namespace rk {
 
 #ifndef RK_THREADS
-#define RK_THREADS 256
+#define RK_THREADS 512
 #endif
 #ifndef RK_MINBLOCKS
-#define RK_MINBLOCKS 2
+#define RK_MINBLOCKS 1
 #endif
 #ifndef RK_RMAX
 #define RK_RMAX 7
@@ -53,8 +53,8 @@ namespace rk {
 #define RK_UNROLL 2
 #endif
 constexpr int kStepUnroll = RK_UNROLL;    // full-step loop unroll
-constexpr int kThreads = RK_THREADS;      // class kernel: 8 warps per CTA
-constexpr int kMinBlocks = RK_MINBLOCKS;  // class kernel: 2 CTAs / SM
+constexpr int kThreads = RK_THREADS;      // class kernel: 16 warps per CTA
+constexpr int kMinBlocks = RK_MINBLOCKS;  // class kernel: 1 CTA / SM (<= 128 registers)
 constexpr unsigned kFull = 0xffffffffu;
 
 // Class encoding: cls = ((len_idx * kNumR) + r_idx) * kNumNck + nc_kind
