@@ -50,6 +50,11 @@ extern "C" {
 #define RK_MODE_EXACT 0
 #define RK_MODE_FAST 1
 
+/* Element types of x and out (engine.py's precision "single" / "double",
+ * features.py:16-24). */
+#define RK_DTYPE_F32 0
+#define RK_DTYPE_F64 1
+
 typedef struct rk_bank_s* rk_bank_t;
 
 /* Summary of a device bank (the dilation-grouped layout). */
@@ -91,19 +96,31 @@ int rk_bank_create(int64_t n_kernels, int32_t n_channels, int32_t l_series,
                    const int32_t* channel_counts, int32_t device,
                    rk_bank_t* bank);
 int rk_bank_destroy(rk_bank_t bank);
+
+/* Attach the float64 parameters (KernelBank.biases / .weights, uncast) for
+ * precision "double" transforms (engine.py:274-276 casts to the compute
+ * dtype, which for "double" is the identity). */
+int rk_bank_attach_f64(rk_bank_t bank, const double* biases, const double* weights);
 int rk_bank_info(rk_bank_t bank, rk_bank_info_t* info);
 
-/* Transform n_series series x[(n_series, n_channels, l_series) float32,
- * C-contiguous] with every kernel of the bank and write rows
- * [row0, row0 + n_series) of out (row stride ld_out floats) in the
- * reference layout: out[row, k*fpk] = ppv_k, out[row, k*fpk + 1] = max_k
- * (features.py:1-5, engine.py:186-188).  fpk is 2 (3 = MPV is not yet
- * supported).  x and out may be host or device pointers.  stream is a
+/* Transform n_series series x[(n_series, n_channels, l_series), C-contiguous,
+ * element type dtype] with every kernel of the bank and write rows
+ * [row0, row0 + n_series) of out (same element type, row stride ld_out
+ * elements) in the reference layout: out[row, k*fpk] = ppv_k,
+ * out[row, k*fpk + 1] = max_k and, for fpk == 3, out[row, k*fpk + 2] = mpv_k
+ * (features.py:1-5, engine.py:186-188, 236-247).  float32 with fpk == 2 runs
+ * the FFMA2 kernels in either mode; float64 or fpk == 3 run the cell kernel
+ * (the reference loop order, exact in both modes).  x and out may be host or
+ * device pointers.  stream is a
  * cudaStream_t (NULL = the library's per-device stream); for device x and
  * out the call is asynchronous on that stream, otherwise it returns after
  * the features are in out.  *executed (may be NULL) receives the number of
  * dot-product positions evaluated, counted on the device; it equals
  * engine.expected_dot_products (engine.py:137-145). */
+int rk_transform(rk_bank_t bank, const void* x, int32_t dtype, int64_t n_series,
+                 void* out, int64_t ld_out, int64_t row0, int32_t fpk,
+                 int32_t mode, void* stream, int64_t* executed);
+/* rk_transform with dtype RK_DTYPE_F32. */
 int rk_transform_f32(rk_bank_t bank, const float* x, int64_t n_series,
                      float* out, int64_t ld_out, int64_t row0, int32_t fpk,
                      int32_t mode, void* stream, int64_t* executed);
@@ -115,7 +132,8 @@ int rk_transform_f32(rk_bank_t bank, const float* x, int64_t n_series,
  * and cached by the identity and content of the bank arrays.  x and out are
  * host pointers (the numpy arrays the engine passes); workers_per_cell is
  * accepted for signature parity and, as in the reference, cannot change
- * the result.  Uses RK_MODE_EXACT so results are byte-identical. */
+ * the result.  fpk 3 adds MPV (_run_batch_mpv, engine.py:193-249).  Uses
+ * RK_MODE_EXACT so results are byte-identical. */
 int64_t rk_run_batch_f32(const float* x, int64_t n_instances,
                          int32_t n_channels, int32_t l_series,
                          const int32_t* lengths, const int32_t* dilations,
@@ -124,6 +142,18 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_instances,
                          const int32_t* chidx, const int64_t* choff,
                          const int32_t* chcnt, int64_t n_kernels,
                          int32_t workers, int32_t fpk, float* out,
+                         int64_t ld_out, int64_t row0);
+
+/* The same for precision "double" (the float64 kernel the reference's
+ * engine runs for precision="double", engine.py:274-276). */
+int64_t rk_run_batch_f64(const double* x, int64_t n_instances,
+                         int32_t n_channels, int32_t l_series,
+                         const int32_t* lengths, const int32_t* dilations,
+                         const int32_t* paddings, const double* biases,
+                         const double* wflat, const int64_t* woff,
+                         const int32_t* chidx, const int64_t* choff,
+                         const int32_t* chcnt, int64_t n_kernels,
+                         int32_t workers, int32_t fpk, double* out,
                          int64_t ld_out, int64_t row0);
 
 /* Release cached banks and per-device buffers (optional at exit). */

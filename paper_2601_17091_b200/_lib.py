@@ -24,6 +24,8 @@ RK_ERR_NO_DEVICE = 5
 RK_MODE_EXACT = 0
 RK_MODE_FAST = 1
 MODES = {"exact": RK_MODE_EXACT, "fast": RK_MODE_FAST}
+RK_DTYPE_F32 = 0
+RK_DTYPE_F64 = 1
 
 # Every symbol include/rocket_b200.h declares.
 EXPORTS = (
@@ -33,8 +35,11 @@ EXPORTS = (
     "rk_bank_create",
     "rk_bank_destroy",
     "rk_bank_info",
+    "rk_bank_attach_f64",
+    "rk_transform",
     "rk_transform_f32",
     "rk_run_batch_f32",
+    "rk_run_batch_f64",
     "rk_release_caches",
 )
 
@@ -107,6 +112,12 @@ def load():
     lib.rk_bank_destroy.argtypes = [p]
     lib.rk_bank_info.restype = ctypes.c_int
     lib.rk_bank_info.argtypes = [p, ctypes.POINTER(BankInfo)]
+    lib.rk_bank_attach_f64.restype = ctypes.c_int
+    lib.rk_bank_attach_f64.argtypes = [p, p, p]
+    lib.rk_transform.restype = ctypes.c_int
+    lib.rk_transform.argtypes = [p, p, i32, i64, p, i64, i64, i32, i32, p, ctypes.POINTER(i64)]
+    lib.rk_run_batch_f64.restype = i64
+    lib.rk_run_batch_f64.argtypes = [p, i64, i32, i32, p, p, p, p, p, p, p, p, p, i64, i32, i32, p, i64, i64]
     lib.rk_transform_f32.restype = ctypes.c_int
     lib.rk_transform_f32.argtypes = [p, p, i64, p, i64, i64, i32, i32, p, ctypes.POINTER(i64)]
     lib.rk_run_batch_f32.restype = i64

@@ -110,6 +110,15 @@ struct rk_bank_s {
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
   int* d_chan_off = nullptr;
+  // cell path (precision "double", MPV): reference-layout parameters
+  rk::CellKernel* d_cell = nullptr;
+  int* d_chidx = nullptr;
+  float* d_cw32 = nullptr;
+  float* d_cb32 = nullptr;
+  double* d_cw64 = nullptr;
+  double* d_cb64 = nullptr;
+  std::vector<int64_t> cell_order;  // sorted position -> bank index
+  int64_t n_weights = 0;
   int64_t device_bytes = 0;
   std::map<std::pair<int, int>, int*> d_block_start;  // (class, n_blocks) -> device boundaries
   std::mutex mu;
@@ -121,6 +130,12 @@ struct rk_bank_s {
     cudaFree(d_chunks);
     cudaFree(d_weights);
     cudaFree(d_chan_off);
+    cudaFree(d_cell);
+    cudaFree(d_chidx);
+    cudaFree(d_cw32);
+    cudaFree(d_cb32);
+    cudaFree(d_cw64);
+    cudaFree(d_cb64);
     for (auto& kv : d_block_start) cudaFree(kv.second);
     cudaSetDevice(prev);
   }
@@ -422,9 +437,43 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   return RK_OK;
 }
 
-int launch(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
-           int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
+// Cell path: precision "double" (esz 8) or MPV (fpk 3).
+int launch_cells(rk_bank_t b, const void* d_x, int esz, int64_t n, void* d_out, int64_t ld_out, int fpk,
+                 cudaStream_t stream, unsigned long long* d_exec) {
+  if (esz == 8 && !b->d_cw64) return fail(RK_ERR_INVALID, "double precision needs rk_bank_attach_f64 first");
+  rk::CellArgs a;
+  a.x = d_x;
+  a.out = d_out;
+  a.ld_out = ld_out;
+  a.n_series = n;
+  a.kernels = b->d_cell;
+  a.weights = esz == 8 ? (const void*)b->d_cw64 : (const void*)b->d_cw32;
+  a.biases = esz == 8 ? (const void*)b->d_cb64 : (const void*)b->d_cb32;
+  a.chidx = b->d_chidx;
+  a.executed = d_exec;
+  a.n_kernels = (int)b->K;
+  a.l_series = b->L;
+  a.n_channels = b->C;
+  a.fpk = fpk;
+  dim3 grid((unsigned)((b->K + 127) / 128), (unsigned)std::min<int64_t>(n, 65535));
+  if (esz == 8) {
+    if (fpk == 3)
+      rk::rocket_cell_kernel<double, true><<<grid, 128, 0, stream>>>(a);
+    else
+      rk::rocket_cell_kernel<double, false><<<grid, 128, 0, stream>>>(a);
+  } else {
+    rk::rocket_cell_kernel<float, true><<<grid, 128, 0, stream>>>(a);
+  }
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_outv, int64_t ld_out, int fpk,
+           int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters, int esz) {
   if (n <= 0) return RK_OK;
+  if (esz == 8 || fpk == 3) return launch_cells(b, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec);
+  const float* d_x = static_cast<const float*>(d_xv);
+  float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
   if (b->warp_path) return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
@@ -799,6 +848,40 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   RK_CUDA(cudaMemcpy(b->d_chunks, dev.data(), sizeof(rk::DevChunk) * dev.size(), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(b->d_weights, wpack.data(), sizeof(float) * wpack.size(), cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(b->d_chan_off, chan_off.data(), sizeof(int) * chan_off.size(), cudaMemcpyHostToDevice));
+  // cell path: kernels sorted by (len*nc, l_out) so warp neighbours share
+  // trip counts; weights in the reference layout
+  {
+    int64_t nw = 0, nci = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      nw = std::max<int64_t>(nw, woff[k] + (int64_t)lengths[k] * chcnt[k]);
+      nci = std::max<int64_t>(nci, choff[k] + chcnt[k]);
+    }
+    b->n_weights = nw;
+    b->cell_order.resize(K);
+    for (int64_t k = 0; k < K; ++k) b->cell_order[k] = k;
+    auto l_out_of = [&](int64_t k) { return (int64_t)L + 2 * paddings[k] - (int64_t)(lengths[k] - 1) * dilations[k]; };
+    std::stable_sort(b->cell_order.begin(), b->cell_order.end(), [&](int64_t x, int64_t y) {
+      const int64_t tx = (int64_t)lengths[x] * chcnt[x], ty = (int64_t)lengths[y] * chcnt[y];
+      if (tx != ty) return tx > ty;
+      return l_out_of(x) > l_out_of(y);
+    });
+    std::vector<rk::CellKernel> ck(K);
+    std::vector<float> cb(K);
+    for (int64_t i = 0; i < K; ++i) {
+      const int64_t k = b->cell_order[i];
+      ck[i] = rk::CellKernel{lengths[k], dilations[k], paddings[k], chcnt[k], (int)l_out_of(k), (int)woff[k],
+                             (int)choff[k], (int)k};
+      cb[i] = biases[k];
+    }
+    RK_CUDA(cudaMalloc(&b->d_cell, sizeof(rk::CellKernel) * K));
+    RK_CUDA(cudaMalloc(&b->d_chidx, sizeof(int) * std::max<int64_t>(1, nci)));
+    RK_CUDA(cudaMalloc(&b->d_cw32, sizeof(float) * std::max<int64_t>(1, nw)));
+    RK_CUDA(cudaMalloc(&b->d_cb32, sizeof(float) * K));
+    RK_CUDA(cudaMemcpy(b->d_cell, ck.data(), sizeof(rk::CellKernel) * K, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(b->d_chidx, chidx, sizeof(int) * nci, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(b->d_cw32, weights, sizeof(float) * nw, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(b->d_cb32, cb.data(), sizeof(float) * K, cudaMemcpyHostToDevice));
+  }
   b->device_bytes = (int64_t)(sizeof(rk::DevChunk) * dev.size() + sizeof(float) * wpack.size() +
                               sizeof(int) * chan_off.size());
   *out = b.release();
@@ -831,11 +914,15 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   return RK_OK;
 }
 
-int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t ld_out, int64_t row0,
-                     int32_t fpk, int32_t mode, void* stream_ptr, int64_t* executed) {
+int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* outv, int64_t ld_out, int64_t row0,
+                 int32_t fpk, int32_t mode, void* stream_ptr, int64_t* executed) {
   if (!b) return fail(RK_ERR_INVALID, "NULL bank");
   if (n < 0 || row0 < 0) return fail(RK_ERR_INVALID, "n_series and row0 must be non-negative");
-  if (fpk != 2) return fail(RK_ERR_UNSUPPORTED, "features_per_kernel=%d: only 2 (ppv, max) is implemented", fpk);
+  if (fpk != 2 && fpk != 3) return fail(RK_ERR_INVALID, "features_per_kernel=%d must be 2 or 3", fpk);
+  if (dtype != RK_DTYPE_F32 && dtype != RK_DTYPE_F64) return fail(RK_ERR_INVALID, "unknown dtype %d", dtype);
+  const int esz = dtype == RK_DTYPE_F64 ? 8 : 4;
+  const char* x = static_cast<const char*>(xv);
+  char* out = static_cast<char*>(outv);
   if (mode != RK_MODE_EXACT && mode != RK_MODE_FAST) return fail(RK_ERR_INVALID, "unknown mode %d", mode);
   if (ld_out < b->K * fpk) return fail(RK_ERR_INVALID, "ld_out %lld < n_kernels * fpk", (long long)ld_out);
   if (executed) *executed = 0;
@@ -855,8 +942,8 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     rc = stream_scratch(st, stream, &d_exec);
     if (rc) return rc;
     RK_CUDA(cudaMemsetAsync(d_exec, 0, sizeof(unsigned long long), stream));
-    rc = launch(b, st, x, n, out + row0 * ld_out, ld_out, fpk, mode, stream, d_exec,
-                reinterpret_cast<int*>(d_exec + 1));
+    rc = launch(b, st, x, n, out + row0 * ld_out * esz, ld_out, fpk, mode, stream, d_exec,
+                reinterpret_cast<int*>(d_exec + 1), esz);
     if (rc) return rc;
     if (executed) {
       unsigned long long h = 0;
@@ -877,8 +964,8 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     ~Release() { release_worker(st, w); }
   } release{st, w};
   cudaStream_t stream = w->stream;
-  const int64_t out_row_bytes = b->K * fpk * 4;
-  const int64_t in_row_bytes = row_in * 4;
+  const int64_t out_row_bytes = b->K * fpk * esz;
+  const int64_t in_row_bytes = row_in * esz;
   const int64_t budget = (int64_t)1 << 30;  // device scratch per output buffer
   int64_t batch = std::max<int64_t>(1, budget / out_row_bytes);
   batch = std::min<int64_t>(batch, n);
@@ -913,7 +1000,7 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
     const int64_t s0 = k * batch, cnt = std::min(batch, n - s0);
     const int ib = (int)(k % kInBufs);
     if (k >= kInBufs) RK_CUDA(cudaStreamWaitEvent(w->h2d_stream, w->in_free[ib], 0));
-    RK_CUDA(cudaMemcpyAsync(w->d_in[ib], x + s0 * row_in, cnt * in_row_bytes, cudaMemcpyHostToDevice,
+    RK_CUDA(cudaMemcpyAsync(w->d_in[ib], x + s0 * in_row_bytes, cnt * in_row_bytes, cudaMemcpyHostToDevice,
                             w->h2d_stream));
     RK_CUDA(cudaEventRecord(w->in_ready[ib], w->h2d_stream));
     return RK_OK;
@@ -929,25 +1016,25 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
       rc = h2d(k + 1);  // enqueued before this batch's D2H
       if (rc) return rc;
     }
-    const float* kx = x + s0 * row_in;
+    const void* kx = x + s0 * in_row_bytes;
     if (!dx) {
       RK_CUDA(cudaStreamWaitEvent(stream, w->in_ready[ib], 0));
       kx = w->d_in[ib];
     }
-    float* ko = dout ? out + (row0 + s0) * ld_out : w->d_out[ob];
+    void* ko = dout ? (void*)(out + (row0 + s0) * ld_out * esz) : (void*)w->d_out[ob];
     const int64_t kld = dout ? ld_out : b->K * fpk;
     if (!dout && k >= kOutBufs) RK_CUDA(cudaStreamWaitEvent(stream, w->out_free[ob], 0));
-    rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec, reinterpret_cast<int*>(d_exec + 1));
+    rc = launch(b, st, kx, cnt, ko, kld, fpk, mode, stream, d_exec, reinterpret_cast<int*>(d_exec + 1), esz);
     if (rc) return rc;
     if (!dx) RK_CUDA(cudaEventRecord(w->in_free[ib], stream));
     if (!dout) {
       RK_CUDA(cudaEventRecord(w->out_ready[ob], stream));
       RK_CUDA(cudaStreamWaitEvent(w->d2h_stream, w->out_ready[ob], 0));
-      float* hdst = out + (row0 + s0) * ld_out;
+      char* hdst = out + (row0 + s0) * ld_out * esz;
       if (ld_out == kld) {
         RK_CUDA(cudaMemcpyAsync(hdst, w->d_out[ob], cnt * out_row_bytes, cudaMemcpyDeviceToHost, w->d2h_stream));
       } else {
-        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * 4, w->d_out[ob], kld * 4, kld * 4, cnt, cudaMemcpyDeviceToHost,
+        RK_CUDA(cudaMemcpy2DAsync(hdst, ld_out * esz, w->d_out[ob], kld * esz, kld * esz, cnt, cudaMemcpyDeviceToHost,
                                   w->d2h_stream));
       }
       RK_CUDA(cudaEventRecord(w->out_free[ob], w->d2h_stream));
@@ -959,6 +1046,23 @@ int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t
   RK_CUDA(cudaStreamSynchronize(w->h2d_stream));
   RK_CUDA(cudaStreamSynchronize(stream));
   if (executed) *executed = (int64_t)h;
+  return RK_OK;
+}
+
+int rk_transform_f32(rk_bank_t b, const float* x, int64_t n, float* out, int64_t ld_out, int64_t row0,
+                     int32_t fpk, int32_t mode, void* stream, int64_t* executed) {
+  return rk_transform(b, x, RK_DTYPE_F32, n, out, ld_out, row0, fpk, mode, stream, executed);
+}
+
+int rk_bank_attach_f64(rk_bank_t b, const double* biases, const double* weights) {
+  if (!b || !biases || !weights) return fail(RK_ERR_INVALID, "NULL bank or array");
+  RK_CUDA(cudaSetDevice(b->device));
+  std::vector<double> cb(b->K);
+  for (int64_t i = 0; i < b->K; ++i) cb[i] = biases[b->cell_order[i]];
+  if (!b->d_cw64) RK_CUDA(cudaMalloc(&b->d_cw64, sizeof(double) * std::max<int64_t>(1, b->n_weights)));
+  if (!b->d_cb64) RK_CUDA(cudaMalloc(&b->d_cb64, sizeof(double) * b->K));
+  RK_CUDA(cudaMemcpy(b->d_cw64, weights, sizeof(double) * b->n_weights, cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpy(b->d_cb64, cb.data(), sizeof(double) * b->K, cudaMemcpyHostToDevice));
   return RK_OK;
 }
 
@@ -986,13 +1090,18 @@ uint64_t fnv(uint64_t h, const void* data, size_t bytes) {
 }
 }  // namespace
 
-int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
-                         const int32_t* dilations, const int32_t* paddings, const float* biases,
-                         const float* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
-                         const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, float* out,
-                         int64_t ld_out, int64_t row0) {
+namespace {
+// Shared body of the stateless entry points: look the bank up in the cache
+// (identity + content of the arrays), build it on a miss, transform.
+int64_t run_batch_impl(int dtype, const void* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                       const int32_t* dilations, const int32_t* paddings, const void* biases, const void* wflat,
+                       const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
+                       int64_t K, int32_t workers, int32_t fpk, void* out, int64_t ld_out, int64_t row0) {
   if (workers < 1) return -fail(RK_ERR_INVALID, "workers_per_cell must be positive");
   if (K < 1) return -fail(RK_ERR_INVALID, "bank must contain at least one kernel");
+  if (!lengths || !dilations || !paddings || !biases || !wflat || !woff || !chidx || !choff || !chcnt)
+    return -fail(RK_ERR_INVALID, "bank array pointer is NULL");
+  const int esz = dtype == RK_DTYPE_F64 ? 8 : 4;
   int64_t nw = 0, nci = 0;
   for (int64_t k = 0; k < K; ++k) {
     nw = std::max<int64_t>(nw, woff[k] + (int64_t)lengths[k] * chcnt[k]);
@@ -1005,13 +1114,13 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, c
   key.K = K;
   key.C = C;
   key.L = L;
-  uint64_t h = 1469598103934665603ull;
+  uint64_t h = 1469598103934665603ull ^ (uint64_t)dtype;
   h = fnv(h, lengths, 4 * K);
   h = fnv(h, dilations, 4 * K);
   h = fnv(h, paddings, 4 * K);
-  h = fnv(h, biases, 4 * K);
+  h = fnv(h, biases, esz * K);
   h = fnv(h, chcnt, 4 * K);
-  h = fnv(h, wflat, 4 * nw);
+  h = fnv(h, wflat, esz * nw);
   h = fnv(h, chidx, 4 * nci);
   key.hash = h;
   rk_bank_t bank = nullptr;
@@ -1023,9 +1132,26 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, c
   if (!bank) {
     int dev = 0;
     cudaGetDevice(&dev);
-    int rc = rk_bank_create(K, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx, choff, chcnt, dev,
-                            &bank);
+    std::vector<float> b32, w32;
+    const float* bf = static_cast<const float*>(biases);
+    const float* wf = static_cast<const float*>(wflat);
+    if (esz == 8) {
+      const double* bd = static_cast<const double*>(biases);
+      const double* wd = static_cast<const double*>(wflat);
+      b32.assign(bd, bd + K);
+      w32.assign(wd, wd + nw);
+      bf = b32.data();
+      wf = w32.data();
+    }
+    int rc = rk_bank_create(K, C, L, lengths, dilations, paddings, bf, wf, woff, chidx, choff, chcnt, dev, &bank);
     if (rc) return -rc;
+    if (esz == 8) {
+      rc = rk_bank_attach_f64(bank, static_cast<const double*>(biases), static_cast<const double*>(wflat));
+      if (rc) {
+        rk_bank_destroy(bank);
+        return -rc;
+      }
+    }
     std::lock_guard<std::mutex> lk(g_cache_mu);
     if (g_cache.size() >= 8) {
       rk_bank_destroy(g_cache.begin()->second);
@@ -1034,9 +1160,28 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, c
     g_cache[key] = bank;
   }
   int64_t executed = 0;
-  int rc = rk_transform_f32(bank, x, n_inst, out, ld_out, row0, fpk, RK_MODE_EXACT, nullptr, &executed);
+  int rc = rk_transform(bank, x, dtype, n_inst, out, ld_out, row0, fpk, RK_MODE_EXACT, nullptr, &executed);
   if (rc) return -rc;
   return executed;
+}
+}  // namespace
+
+int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                         const int32_t* dilations, const int32_t* paddings, const float* biases,
+                         const float* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
+                         const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, float* out,
+                         int64_t ld_out, int64_t row0) {
+  return run_batch_impl(RK_DTYPE_F32, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0);
+}
+
+int64_t rk_run_batch_f64(const double* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                         const int32_t* dilations, const int32_t* paddings, const double* biases,
+                         const double* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
+                         const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, double* out,
+                         int64_t ld_out, int64_t row0) {
+  return run_batch_impl(RK_DTYPE_F64, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0);
 }
 
 int rk_release_caches(void) {

@@ -635,3 +635,101 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
 }
 
 }  // namespace rk
+
+// ---------------------------------------------------------------------------
+// Cell kernel: one thread per (series, kernel) cell, the reference's loop
+// verbatim (engine.py:157-188 and the MPV variant engine.py:202-247):
+// positions ascending, channels then taps ascending, out-of-range taps
+// skipped, RN(acc + RN(w*x)) without contraction, bias last, the positive
+// sum accumulated in position order.  Used for precision "double" and for
+// MPV (fpk = 3), where the ordered positive sum leaves no room for the
+// reordered fast path.  Kernels are visited in a (length, channels, l_out)
+// sorted order so a warp's threads run similar trip counts.
+namespace rk {
+
+struct __align__(16) CellKernel {
+  int len, d, p, nc;
+  int l_out, woff, choff, col;
+};
+static_assert(sizeof(CellKernel) == 32, "CellKernel layout");
+
+struct CellArgs {
+  const void* x;         // (n, C, L) of T, device
+  void* out;             // row 0 of this launch
+  int64_t ld_out;
+  int64_t n_series;
+  const CellKernel* kernels;
+  const void* weights;   // T, reference layout (channel-major per kernel)
+  const void* biases;    // T, per sorted kernel
+  const int* chidx;
+  unsigned long long* executed;
+  int n_kernels;
+  int l_series;
+  int n_channels;
+  int fpk;
+};
+
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T from_double(double v);
+template <>
+__device__ __forceinline__ float from_double<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ double from_double<double>(double v) { return v; }
+
+template <typename T, bool MPV>
+__global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
+  const int ks = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = ks < a.n_kernels;
+  const CellKernel kd = live ? a.kernels[ks] : CellKernel{7, 1, 0, 1, 0, 0, 0, 0};
+  const T* w = reinterpret_cast<const T*>(a.weights) + kd.woff;
+  const T bias = live ? reinterpret_cast<const T*>(a.biases)[ks] : T(0);
+  const int L = a.l_series, C = a.n_channels;
+  unsigned long long done = 0;
+  for (int64_t i = blockIdx.y; i < a.n_series; i += gridDim.y) {
+    const T* xi = reinterpret_cast<const T*>(a.x) + i * (int64_t)C * L;
+    int64_t count = 0;
+    T running_max = -INFINITY;
+    T psum = T(0);
+    for (int t = 0; t < kd.l_out; ++t) {
+      T acc = T(0);
+      for (int c = 0; c < kd.nc; ++c) {
+        const T* xc = xi + (int64_t)__ldg(a.chidx + kd.choff + c) * L;
+        const T* wr = w + c * kd.len;
+        for (int j = 0; j < kd.len; ++j) {
+          const int idx = t - kd.p + j * kd.d;
+          if (idx >= 0 && idx < L) acc = add_rn<T>(acc, mul_rn<T>(__ldg(wr + j), __ldg(xc + idx)));
+        }
+      }
+      acc = add_rn<T>(acc, bias);
+      if (acc > T(0)) {
+        count += 1;
+        if (MPV) psum = add_rn<T>(psum, acc);
+      }
+      if (acc > running_max) running_max = acc;
+    }
+    if (live) {
+      T* o = reinterpret_cast<T*>(a.out) + i * a.ld_out + (int64_t)kd.col * a.fpk;
+      o[0] = from_double<T>((double)count / (double)kd.l_out);
+      o[1] = running_max;
+      if (MPV) o[2] = count > 0 ? from_double<T>((double)psum / (double)count) : T(0);
+      done += (unsigned long long)kd.l_out;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(kFull, done, o);
+  if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.executed, done);
+}
+
+}  // namespace rk

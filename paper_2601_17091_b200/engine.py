@@ -8,11 +8,13 @@ to hand-written sm_100a kernels.  There is no CPU fallback: without the
 built library or a B200 the calls raise.
 
 Arithmetic modes (keyword-only ``mode``):
-  "exact" (default) — bit-identical to the reference's single-precision
-                      engine (tap order, bias last, no FMA contraction);
+  "exact" (default) — bit-identical to the reference engine (tap order,
+                      bias last, no FMA contraction);
   "fast"            — FFMA2 with the bias folded in; within the north-star
                       tolerance (MAX 1e-5 relative, PPV exact except for
                       outputs within 1e-6 of zero).
+precision="double" and include_mpv=True run the cell kernel, which follows
+the reference loop order exactly in both modes (engine.py:193-249).
 """
 
 import ctypes
@@ -236,6 +238,7 @@ class DeviceBank:
         )
         _lib.check(rc, "rk_bank_create")
         self._handle = handle
+        self._f64 = False
         info = _lib.BankInfo()
         _lib.check(lib.rk_bank_info(handle, ctypes.byref(info)), "rk_bank_info")
         self.info = {f: getattr(info, f) for f, _ in _lib.BankInfo._fields_}
@@ -244,16 +247,31 @@ class DeviceBank:
     def handle(self):
         return self._handle
 
-    def transform_into(self, x_ptr, n_series, out_ptr, ld_out, row0=0, mode="exact", stream=None, fpk=2):
+    def attach_f64(self):
+        """Upload the float64 bank parameters (precision "double")."""
+        if not self._f64:
+            bank = self.bank
+            self._keep["biases64"] = np.ascontiguousarray(bank.biases, dtype=np.float64)
+            self._keep["weights64"] = np.ascontiguousarray(bank.weights, dtype=np.float64)
+            rc = _lib.load().rk_bank_attach_f64(self._handle, _ptr(self._keep["biases64"]),
+                                                _ptr(self._keep["weights64"]))
+            _lib.check(rc, "rk_bank_attach_f64")
+            self._f64 = True
+
+    def transform_into(self, x_ptr, n_series, out_ptr, ld_out, row0=0, mode="exact", stream=None, fpk=2,
+                       precision="single"):
         """Raw-pointer transform (host or device pointers); returns the
         device-counted executed positions."""
         lib = _lib.load()
+        dtype = _lib.RK_DTYPE_F64 if precision == "double" else _lib.RK_DTYPE_F32
+        if dtype == _lib.RK_DTYPE_F64:
+            self.attach_f64()
         executed = ctypes.c_int64(0)
-        rc = lib.rk_transform_f32(
-            self._handle, ctypes.c_void_p(x_ptr), int(n_series), ctypes.c_void_p(out_ptr), int(ld_out),
+        rc = lib.rk_transform(
+            self._handle, ctypes.c_void_p(x_ptr), dtype, int(n_series), ctypes.c_void_p(out_ptr), int(ld_out),
             int(row0), int(fpk), _lib.MODES[mode], ctypes.c_void_p(stream or 0), ctypes.byref(executed),
         )
-        _lib.check(rc, "rk_transform_f32")
+        _lib.check(rc, "rk_transform")
         return int(executed.value)
 
     def close(self):
@@ -287,24 +305,20 @@ def device_bank(bank: KernelBank, device: int = 0) -> DeviceBank:
         return db
 
 
-def _check_request(include_mpv, precision, mode):
+def _check_request(precision, mode):
     precision_dtype(precision)
     if mode not in _lib.MODES:
         raise ValueError(f"mode must be one of {sorted(_lib.MODES)}")
-    if include_mpv:
-        raise NotImplementedError("include_mpv=True (fpk=3) is not implemented on the CUDA path yet")
-    if precision != "single":
-        raise NotImplementedError("precision='double' is not implemented on the CUDA path yet")
 
 
-def _run_range(x, dbank, limits, out, row0, stats, mode):
+def _run_range(x, dbank, limits, out, row0, stats, mode, fpk, precision):
     """engine.py:271-296: the batch loop, each batch one C-ABI call."""
     plan = plan_batches(x.shape[0], bytes_per_instance(x.shape[1], x.shape[2]), limits)
-    row_floats = x.shape[1] * x.shape[2]
+    row_bytes = x.shape[1] * x.shape[2] * x.itemsize
     for start, count in plan.batches:
         stats.total_dot_products += dbank.transform_into(
-            x.ctypes.data + start * row_floats * SINGLE_BYTES, count, out.ctypes.data, out.shape[1],
-            row0 + start, mode=mode,
+            x.ctypes.data + start * row_bytes, count, out.ctypes.data, out.shape[1], row0 + start, mode=mode,
+            fpk=fpk, precision=precision,
         )
         stats.n_batches += 1
 
@@ -324,13 +338,14 @@ def transform_with_stats(
     limits = GridLimits() if limits is None else limits
     values = np.asarray(getattr(data, "values", data))
     _check_shapes(values, bank, limits)
-    _check_request(include_mpv, precision, mode)
-    fpk = 2
-    x = np.ascontiguousarray(values, dtype=np.float32)
-    out = np.empty((values.shape[0], bank.count * fpk), dtype=np.float32)
+    _check_request(precision, mode)
+    dtype = precision_dtype(precision)
+    fpk = 3 if include_mpv else 2
+    x = np.ascontiguousarray(values, dtype=dtype)
+    out = np.empty((values.shape[0], bank.count * fpk), dtype=dtype)
     stats = TransformStats()
     if values.shape[0]:
-        _run_range(x, device_bank(bank, device), limits, out, 0, stats, mode)
+        _run_range(x, device_bank(bank, device), limits, out, 0, stats, mode, fpk, precision)
     matrix = FeatureMatrix(values=out, n_kernels=bank.count, features_per_kernel=fpk, precision=precision)
     return matrix, stats
 
@@ -368,10 +383,11 @@ def transform_sharded(
     limits = GridLimits() if limits is None else limits
     values = np.asarray(getattr(data, "values", data))
     _check_shapes(values, bank, limits)
-    _check_request(include_mpv, precision, mode)
-    fpk = 2
-    x = np.ascontiguousarray(values, dtype=np.float32)
-    out = np.empty((values.shape[0], bank.count * fpk), dtype=np.float32)
+    _check_request(precision, mode)
+    dtype = precision_dtype(precision)
+    fpk = 3 if include_mpv else 2
+    x = np.ascontiguousarray(values, dtype=dtype)
+    out = np.empty((values.shape[0], bank.count * fpk), dtype=dtype)
     shards = [(s, c) for s, c in plan_shards(values.shape[0], n_devices) if c]
     if shards:
         if devices is None:
@@ -383,7 +399,8 @@ def transform_sharded(
             start, count = shard
             try:
                 st = TransformStats()
-                _run_range(x[start : start + count], device_bank(bank, dev), limits, out, start, st, mode)
+                _run_range(x[start : start + count], device_bank(bank, dev), limits, out, start, st, mode, fpk,
+                           precision)
             except BaseException as e:  # re-raised on the caller thread
                 errors.append(e)
 

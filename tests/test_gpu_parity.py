@@ -176,3 +176,53 @@ def test_errors_mirror_reference(cuda_ready):
     big = generate_bank(200_000, 1, 4, GenOptions(seed=3))
     with pytest.raises(CapacityError):
         transform(np.zeros((1, 1, 200_000), dtype=np.float32), big)
+
+
+OTHER = [(name, v) for name, case in gc.CASES.items() for v in case["variants"] if v != "single"]
+
+
+@pytest.mark.parametrize("name,variant", OTHER)
+def test_double_and_mpv_bytes_match_reference(name, variant, golden_transforms, cuda_ready):
+    """precision="double" and include_mpv=True (the cell kernel) in both modes."""
+    values, bank = _case(name)
+    precision = variant.split("_")[0]
+    mpv = variant.endswith("_mpv")
+    ref = golden_transforms[f"{name}/{variant}"]
+    for mode in ("exact", "fast"):
+        fm, stats = transform_with_stats(values, bank, include_mpv=mpv, precision=precision, mode=mode)
+        assert fm.values.dtype == ref.dtype and fm.values.shape == ref.shape
+        assert fm.values.tobytes() == ref.tobytes()
+        assert stats.total_dot_products == int(golden_transforms[f"{name}/{variant}/executed"][0])
+
+
+def test_mpv_and_double_config2_rows_vs_oracle(cuda_ready):
+    """MPV (single) and double precision at the BASELINE L=1024 / 10k shape."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(1024, 1, 10000, GenOptions(seed=0))
+    values = synth_random(8, 1, 1024, seed=1).values
+    mpv = transform(values, bank, include_mpv=True).values
+    assert mpv.tobytes() == oracle_transform(values, bank, include_mpv=True).tobytes()
+    dbl = transform(values, bank, precision="double").values
+    assert dbl.tobytes() == oracle_transform(values, bank, precision="double").tobytes()
+
+
+def test_run_batch_f64_dropin(golden_transforms, cuda_ready):
+    lib = cuda_ready
+    values, bank = _case("rc5")
+    x = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty((x.shape[0], bank.count * 2), dtype=np.float64)
+    a = dict(
+        lengths=bank.lengths, dilations=bank.dilations, paddings=bank.paddings, biases=bank.biases,
+        wflat=bank.weights, woff=bank.weight_offsets, chidx=bank.channel_indices, choff=bank.channel_offsets,
+        chcnt=bank.channel_counts,
+    )
+    a = {k: np.ascontiguousarray(v) for k, v in a.items()}
+    p = lambda arr: arr.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    executed = lib.rk_run_batch_f64(
+        p(x), x.shape[0], x.shape[1], x.shape[2], p(a["lengths"]), p(a["dilations"]), p(a["paddings"]),
+        p(a["biases"]), p(a["wflat"]), p(a["woff"]), p(a["chidx"]), p(a["choff"]), p(a["chcnt"]),
+        bank.count, 7, 2, p(out), out.shape[1], 0,
+    )
+    assert executed == expected_dot_products(bank, x.shape[0])
+    assert out.tobytes() == golden_transforms["rc5/double"].tobytes()
