@@ -248,6 +248,7 @@ void fill_r(KernelFn* t, int li) {
   fill_nck<LEN, rk::r_of(1)>(t, li, 1);
   fill_nck<LEN, rk::r_of(2)>(t, li, 2);
   fill_nck<LEN, rk::r_of(3)>(t, li, 3);
+  fill_nck<LEN, rk::r_of(4)>(t, li, 4);
 }
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
@@ -323,6 +324,7 @@ void wfill_r(WarpFn* t, int li) {
   wfill_nck<LEN, rk::r_of(1)>(t, li, 1);
   wfill_nck<LEN, rk::r_of(2)>(t, li, 2);
   wfill_nck<LEN, rk::r_of(3)>(t, li, 3);
+  wfill_nck<LEN, rk::r_of(4)>(t, li, 4);
 }
 struct WarpTable {
   WarpFn fn[2 * rk::kNumClasses] = {};
@@ -356,6 +358,16 @@ bool is_device_pointer(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// The class a launch executes: exact mode runs the largest-R class with the
+// R = 7 instantiation (same chunks, only positions per lane differ).
+int exec_cls(int cls, int exact) {
+  const int nck = cls % rk::kNumNck;
+  const int ri = (cls / rk::kNumNck) % rk::kNumR;
+  const int li = cls / (rk::kNumNck * rk::kNumR);
+  const int r = exact ? std::min(ri, rk::kExactRIdxCap) : ri;
+  return (li * rk::kNumR + r) * rk::kNumNck + nck;
+}
+
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
 // Enqueue the transform of n series already on the device: one launch per
@@ -373,7 +385,7 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->warp_launches.size(); ++li) {
     const auto& wl = b->warp_launches[li];
-    WarpFn fn = warp_table().fn[2 * wl.cls + exact];
+    WarpFn fn = warp_table().fn[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (KernelFn)fn, smem);
     if (rc) return rc;
@@ -488,7 +500,7 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
   for (int cls = 0; cls < rk::kNumClasses; ++cls) {
     const int nchunks = b->cls_end[cls] - b->cls_begin[cls];
     if (nchunks <= 0) continue;
-    KernelFn fn = kernel_table().fn[2 * cls + exact];
+    KernelFn fn = kernel_table().fn[2 * exec_cls(cls, exact) + exact];
     // Stage several series per item when the class is too small to keep
     // all warps of a CTA busy on one series.
     int spi = 1;

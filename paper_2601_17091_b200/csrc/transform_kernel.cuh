@@ -47,7 +47,7 @@ namespace rk {
 #define RK_MINBLOCKS 1
 #endif
 #ifndef RK_RMAX
-#define RK_RMAX 7
+#define RK_RMAX 11
 #endif
 #ifndef RK_UNROLL
 #define RK_UNROLL 2
@@ -60,10 +60,12 @@ constexpr unsigned kFull = 0xffffffffu;
 // Class encoding: cls = ((len_idx * kNumR) + r_idx) * kNumNck + nc_kind
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
 //           2: >= 3 channels (generic); 3: 1 channel, 1 pair
-constexpr int kNumR = 4;
-// positions per lane of class r_idx: 1, 3, 5, RK_RMAX (odd: spreads lanes
-// over the shared-memory banks)
-__host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 3 ? RK_RMAX : 2 * r_idx + 1; }
+constexpr int kNumR = 5;
+// positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX (odd: spreads lanes
+// over the shared-memory banks).  Exact-mode launches run the RK_RMAX class
+// with the R = 7 kernel (its FMUL2 temporaries leave no room for 11).
+__host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 4 ? RK_RMAX : 2 * r_idx + 1; }
+constexpr int kExactRIdxCap = 3;
 constexpr int kNumNck = 4;
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
