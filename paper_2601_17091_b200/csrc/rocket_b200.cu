@@ -408,7 +408,7 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     h.vec_out = (fpk == 2 && (ld_out % 2) == 0 && ((uintptr_t)d_out % 8) == 0) ? 1 : 0;
     h.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
     h.one = 1.0f;
-    h.wbytes = (NC * P * len * 8 + 15) / 16 * 16;
+    h.wbytes = NC * P * len * 8;
     std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -808,7 +808,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         const int nck = cls % rk::kNumNck;
         const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
         const int len = 7 + 2 * (cls / (rk::kNumNck * rk::kNumR));
-        const int wbytes = (NC * P * len * 8 + 15) / 16 * 16;  // 16-byte blocks (LDCU.128)
+        const int wbytes = NC * P * len * 8;
         const int per_chunk = (int)sizeof(rk::WChunk) + wbytes;
         const int cap = (rk::kBlobFloat4 * 16) / per_chunk;
         for (int i0 = cb; i0 < ce; i0 += cap) {
@@ -837,8 +837,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
             wc.r32 = (short)c.r32;
             wc.invd = c.invd;
             std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
-            std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs,
-                        (size_t)NC * P * len * 8);
+            std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
             wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
           }
           b->warp_launches.push_back(std::move(wl));

@@ -152,20 +152,13 @@ __device__ __forceinline__ void accumulate(float2 (&acc)[P][R], const float2 (&w
   }
 }
 
-// dv is the dilation in a vector register (see run_positions): the window
-// addresses are one pointer walked by a register stride (ALU adds), instead
-// of per-load shifts of a uniform value ptxas would first copy into vector
-// registers.
 template <int LEN, int R>
 __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const float* __restrict__ chan, int u0,
-                                            int dv) {
+                                            int d) {
   constexpr int C = (LEN - 1) / 2;
-  const float* p = chan + (u0 - C * dv);
+  const float* p = chan + (u0 - C * d);
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) {
-    xw[q] = *p;
-    p += dv;
-  }
+  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
 }
 
 // Masked steps: positions past n read past the staged row; only the upper
@@ -173,14 +166,11 @@ __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const floa
 // where p_C is the padding of the chunk's longest kernel).
 template <int LEN, int R>
 __device__ __forceinline__ void load_window_clamped(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
-                                                    int u0, int dv, int hi_clamp) {
+                                                    int u0, int d, int hi_clamp) {
   constexpr int C = (LEN - 1) / 2;
-  int i = u0 - C * dv;
+  const int i0 = u0 - C * d;
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) {
-    xw[q] = chan[min(i, hi_clamp)];
-    i += dv;
-  }
+  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(i0 + q * d, hi_clamp)];
 }
 
 // Per-lane pooled state for the kernels of one chunk.  ext is the running
@@ -292,8 +282,8 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
 template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
-                                           const float2 (&init)[P], float2 one2, int u0, int d, int dv,
-                                           int nleft, int hi_clamp, bool live) {
+                                           const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
+                                           int hi_clamp, bool live) {
   // FAST masked steps start dead positions at +inf: inf + finite stays
   // +inf, which has a clear sign bit (not counted) and never lowers the min
   float2 init_r[P][R];
@@ -313,9 +303,9 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
   for (int s = 0; s < NC; ++s) {
     float xw[R + LEN - 1];
     if (MASKED)
-      load_window_clamped<LEN, R>(xw, chan[s], u0, dv, hi_clamp);
+      load_window_clamped<LEN, R>(xw, chan[s], u0, d, hi_clamp);
     else
-      load_window<LEN, R>(xw, chan[s], u0, dv);
+      load_window<LEN, R>(xw, chan[s], u0, d);
     if (s == 0)
       accumulate<LEN, R, P, EXACT, true>(acc, w[s], xw, init_r, one2);
     else
@@ -348,15 +338,12 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   int a = (int)((lane + 0.5f) * invd);
   int s = lane - a * d;
   int v0 = a * RD + s;
-  const int dstep = q32 * RD + r32;
-  // the dilation as a vector-register value (a shuffle hides its
-  // uniformity from ptxas) for the window address walks
-  const int dvec = __shfl_sync(kFull, d, 0);
+  const int dv = q32 * RD + r32;
 #pragma unroll(kStepUnroll)
   for (int stp = 0; stp < nfull; ++stp) {
-    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, dvec, n, 0, true);
+    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, true);
     s += r32;
-    v0 += dstep;
+    v0 += dv;
     if (s >= d) {
       s -= d;
       v0 += RD - d;
@@ -365,10 +352,9 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   for (int base = nfull << 5; base < starts; base += 32) {
     const bool live = base + lane < starts;
     const int vv = live ? v0 : 0;
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + vv, d, dvec, n - vv, hi_clamp,
-                                          live);
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + vv, d, n - vv, hi_clamp, live);
     s += r32;
-    v0 += dstep;
+    v0 += dv;
     if (s >= d) {
       s -= d;
       v0 += RD - d;
@@ -625,28 +611,14 @@ __global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const _
     float* orow = p.h.out + (int64_t)item * p.h.ld_out;
     for (int ci = 0; ci < p.h.n_chunks; ++ci) {
       const WChunk& c = chunks[ci];
-      // 128-bit parameter loads (LDCU.128): two float2 taps per load
-      const float4* wp4 = reinterpret_cast<const float4*>(wbase + (size_t)ci * p.h.wbytes);
-      constexpr int NW = NC * P * LEN;
-      float wf[2 * NW + 2];
-#pragma unroll
-      for (int f = 0; f < (NW + 1) / 2; ++f) {
-        const float4 v = wp4[f];
-        wf[4 * f] = v.x;
-        wf[4 * f + 1] = v.y;
-        if (4 * f + 2 < 2 * NW + 2) wf[4 * f + 2] = v.z;
-        if (4 * f + 3 < 2 * NW + 2) wf[4 * f + 3] = v.w;
-      }
+      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
       float2 w[NC][P][LEN];
 #pragma unroll
       for (int s = 0; s < NC; ++s)
 #pragma unroll
         for (int q = 0; q < P; ++q)
 #pragma unroll
-          for (int j = 0; j < LEN; ++j) {
-            const int f = (s * P + q) * LEN + j;
-            w[s][q][j] = make_float2(wf[2 * f], wf[2 * f + 1]);
-          }
+          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
       const float* chan[NC];
 #pragma unroll
       for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
