@@ -37,6 +37,10 @@ CONFIGS = {
                     workload="ROCKET transform, 10,000 kernels, 20,000 series x length 16,384"),
     "config5": dict(n=50_000, c=3, l=2048, k=10_000,
                     workload="ROCKET transform, multivariate 3 channels, 50,000 series x length 2,048"),
+    "uni2048": dict(n=50_000, c=1, l=2048, k=10_000,
+                    workload="ROCKET transform, 10,000 kernels, 50,000 series x length 2,048"),
+    "forda": dict(n=3_601, c=1, l=500, k=10_000,
+                  workload="ROCKET transform, 10,000 kernels, 3,601 series x length 500 (FordA shape)"),
 }
 METRIC = "ROCKET transform series/sec (10k kernels, L=1024)"
 FP32_PEAK_MEASURED = 74.0  # TFLOP/s, FFMA2 microbenchmark (profiles/r01_fp32_peak_microbench.jsonl)
