@@ -46,7 +46,7 @@ EXPORTS = (
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     # IEEE float semantics are part of the parity contract: no fast math,
     # keep denormals, IEEE division.
     "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
@@ -72,14 +72,28 @@ class BankInfo(ctypes.Structure):
 
 def build(verbose=False, out=None, defines=()):
     """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles
-    without a GPU)."""
+    without a GPU): the host runtime and the three per-length kernel units
+    are compiled in parallel, then linked into one shared library."""
     out = out or LIB_PATH
-    os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", out,
-           os.path.join(CSRC, "rocket_b200.cu")]
+    objdir = os.path.join(os.path.dirname(out), "obj_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE]
+    units = [("rocket_b200.o", os.path.join(CSRC, "rocket_b200.cu"), [])]
+    units += [(f"kernels_len{n}.o", os.path.join(CSRC, "kernels_len.cu"), [f"-DRK_LEN={n}"]) for n in (7, 9, 11)]
+    procs = []
+    for obj, src, extra in units:
+        cmd = ["nvcc", *flags, *extra, "-c", "-o", os.path.join(objdir, obj), src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    failed = [cmd for cmd, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
+    link = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out,
+            *[os.path.join(objdir, obj) for obj, _, _ in units]]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     return out
 
 

@@ -1,0 +1,47 @@
+// kernels_len.cu — instantiates every kernel of one tap length (RK_LEN)
+// and exports the table filler declared in kernel_tables.h.
+#include "kernel_tables.h"
+
+#ifndef RK_LEN
+#error "compile with -DRK_LEN=7|9|11"
+#endif
+
+namespace {
+constexpr int kLenIdx = (RK_LEN - 7) / 2;
+
+template <int R, int NCK>
+void fill_class(rk::KernelFn* t, int cls) {
+  t[2 * cls + 0] = rk::rocket_class_kernel<RK_LEN, R, NCK, false>;
+  t[2 * cls + 1] = rk::rocket_class_kernel<RK_LEN, R, NCK, true>;
+}
+
+template <int R, int P, int NC>
+void fill_warp(rk::WarpFn* t, int cls) {
+  t[2 * cls + 0] = rk::rocket_warp_kernel<RK_LEN, R, P, NC, false>;
+  t[2 * cls + 1] = rk::rocket_warp_kernel<RK_LEN, R, P, NC, true>;
+}
+
+template <int RI>
+void fill_r(rk::KernelFn* ct, rk::WarpFn* wt) {
+  constexpr int R = rk::r_of(RI);
+  const int base = (kLenIdx * rk::kNumR + RI) * rk::kNumNck;
+  fill_class<R, 0>(ct, base + 0);
+  fill_class<R, 1>(ct, base + 1);
+  fill_class<R, 3>(ct, base + 3);
+  if constexpr (R == 1) fill_class<R, 2>(ct, base + 2);  // generic channels: 1 position per lane
+  fill_warp<R, 2, 1>(wt, base + 0);
+  fill_warp<R, 1, 2>(wt, base + 1);
+  fill_warp<R, 1, 1>(wt, base + 3);
+}
+}  // namespace
+
+#define RK_CAT2(a, b) a##b
+#define RK_CAT(a, b) RK_CAT2(a, b)
+
+void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* wt) {
+  fill_r<0>(ct, wt);
+  fill_r<1>(ct, wt);
+  fill_r<2>(ct, wt);
+  fill_r<3>(ct, wt);
+  fill_r<4>(ct, wt);
+}

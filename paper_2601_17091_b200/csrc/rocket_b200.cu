@@ -8,6 +8,7 @@
 //    engine._run_batch (engine.py:148-190, called at engine.py:280-295).
 #include "../../include/rocket_b200.h"
 #include "transform_kernel.cuh"
+#include "kernel_tables.h"
 
 #include <cuda_runtime.h>
 
@@ -105,9 +106,7 @@ struct rk_bank_s {
     std::vector<rk::float4_t> blob;
   };
   bool warp_path = false;  // one-warp CTAs, parameter-block launches
-  bool cta_path = false;   // same launches, W warps share one staged series
   int warp_ctas_per_sm = 0;
-  int cta_warps = 0;
   std::vector<WarpLaunch> warp_launches;
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
@@ -229,35 +228,17 @@ int device_state(int device, DeviceState** out) {
   return RK_OK;
 }
 
-// Kernel table: one instantiation per (class, mode).
-using KernelFn = void (*)(const rk::LaunchArgs);
-template <int LEN, int R, int NCK>
-void fill_modes(KernelFn* t, int cls) {
-  t[2 * cls + 0] = rk::rocket_class_kernel<LEN, R, NCK, false>;
-  t[2 * cls + 1] = rk::rocket_class_kernel<LEN, R, NCK, true>;
-}
-template <int LEN, int R>
-void fill_nck(KernelFn* t, int li, int ri) {
-  const int base = (li * rk::kNumR + ri) * rk::kNumNck;
-  fill_modes<LEN, R, 0>(t, base + 0);
-  fill_modes<LEN, R, 1>(t, base + 1);
-  fill_modes<LEN, R, 3>(t, base + 3);
-  if constexpr (R == 1) fill_modes<LEN, R, 2>(t, base + 2);  // generic path: 1 position per lane
-}
-template <int LEN>
-void fill_r(KernelFn* t, int li) {
-  fill_nck<LEN, rk::r_of(0)>(t, li, 0);
-  fill_nck<LEN, rk::r_of(1)>(t, li, 1);
-  fill_nck<LEN, rk::r_of(2)>(t, li, 2);
-  fill_nck<LEN, rk::r_of(3)>(t, li, 3);
-  fill_nck<LEN, rk::r_of(4)>(t, li, 4);
-}
+// Kernel tables: one instantiation per (class, mode), compiled per kernel
+// length in kernels_len.cu (three translation units, built in parallel).
+using rk::KernelFn;
+using rk::WarpFn;
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
+  WarpFn wfn[2 * rk::kNumClasses] = {};
   KernelTable() {
-    fill_r<7>(fn, 0);
-    fill_r<9>(fn, 1);
-    fill_r<11>(fn, 2);
+    rk_fill_tables_7(fn, wfn);
+    rk_fill_tables_9(fn, wfn);
+    rk_fill_tables_11(fn, wfn);
   }
 };
 const KernelTable& kernel_table() {
@@ -308,70 +289,6 @@ void release_worker(DeviceState* st, Worker* w) {
   st->free_workers.push_back(w);
 }
 
-// Warp-path kernel table: (class, mode) -> rocket_warp_kernel instance.
-using WarpFn = void (*)(const rk::WParams);
-template <int LEN, int R>
-void wfill_nck(WarpFn* t, int li, int ri) {
-  const int base = (li * rk::kNumR + ri) * rk::kNumNck;
-  t[2 * (base + 0) + 0] = rk::rocket_warp_kernel<LEN, R, 2, 1, false>;
-  t[2 * (base + 0) + 1] = rk::rocket_warp_kernel<LEN, R, 2, 1, true>;
-  t[2 * (base + 1) + 0] = rk::rocket_warp_kernel<LEN, R, 1, 2, false>;
-  t[2 * (base + 1) + 1] = rk::rocket_warp_kernel<LEN, R, 1, 2, true>;
-  t[2 * (base + 3) + 0] = rk::rocket_warp_kernel<LEN, R, 1, 1, false>;
-  t[2 * (base + 3) + 1] = rk::rocket_warp_kernel<LEN, R, 1, 1, true>;
-}
-template <int LEN>
-void wfill_r(WarpFn* t, int li) {
-  wfill_nck<LEN, rk::r_of(0)>(t, li, 0);
-  wfill_nck<LEN, rk::r_of(1)>(t, li, 1);
-  wfill_nck<LEN, rk::r_of(2)>(t, li, 2);
-  wfill_nck<LEN, rk::r_of(3)>(t, li, 3);
-  wfill_nck<LEN, rk::r_of(4)>(t, li, 4);
-}
-struct WarpTable {  // also the type of the CTA-path table
-  WarpFn fn[2 * rk::kNumClasses] = {};
-  WarpTable() {
-    wfill_r<7>(fn, 0);
-    wfill_r<9>(fn, 1);
-    wfill_r<11>(fn, 2);
-  }
-};
-const WarpTable& warp_table() {
-  static WarpTable t;
-  return t;
-}
-
-template <int LEN, int R>
-void cfill_nck(WarpFn* t, int li, int ri) {
-  const int base = (li * rk::kNumR + ri) * rk::kNumNck;
-  t[2 * (base + 0) + 0] = rk::rocket_cta_kernel<LEN, R, 2, 1, false>;
-  t[2 * (base + 0) + 1] = rk::rocket_cta_kernel<LEN, R, 2, 1, true>;
-  t[2 * (base + 1) + 0] = rk::rocket_cta_kernel<LEN, R, 1, 2, false>;
-  t[2 * (base + 1) + 1] = rk::rocket_cta_kernel<LEN, R, 1, 2, true>;
-  t[2 * (base + 3) + 0] = rk::rocket_cta_kernel<LEN, R, 1, 1, false>;
-  t[2 * (base + 3) + 1] = rk::rocket_cta_kernel<LEN, R, 1, 1, true>;
-}
-template <int LEN>
-void cfill_r(WarpFn* t, int li) {
-  cfill_nck<LEN, rk::r_of(0)>(t, li, 0);
-  cfill_nck<LEN, rk::r_of(1)>(t, li, 1);
-  cfill_nck<LEN, rk::r_of(2)>(t, li, 2);
-  cfill_nck<LEN, rk::r_of(3)>(t, li, 3);
-  cfill_nck<LEN, rk::r_of(4)>(t, li, 4);
-}
-struct CtaTable {
-  WarpFn fn[2 * rk::kNumClasses] = {};
-  CtaTable() {
-    cfill_r<7>(fn, 0);
-    cfill_r<9>(fn, 1);
-    cfill_r<11>(fn, 2);
-  }
-};
-const CtaTable& cta_table() {
-  static CtaTable t;
-  return t;
-}
-
 int set_kernel_smem(DeviceState* st, KernelFn fn, int bytes) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   auto it = st->attr_smem.find((const void*)fn);
@@ -415,12 +332,10 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   std::lock_guard<std::mutex> lk(params_mu);
   const int smem = b->smem_bytes;
   const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * b->warp_ctas_per_sm);
-  const int block = 32 * b->cta_warps;
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->warp_launches.size(); ++li) {
     const auto& wl = b->warp_launches[li];
-    const WarpFn* tab = b->cta_path ? cta_table().fn : warp_table().fn;
-    WarpFn fn = tab[2 * exec_cls(wl.cls, exact) + exact];
+    WarpFn fn = kernel_table().wfn[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (KernelFn)fn, smem);
     if (rc) return rc;
@@ -447,7 +362,7 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(block);
+    cfg.blockDim = dim3(32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -522,8 +437,7 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
-  if (b->warp_path || b->cta_path)
-    return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
+  if (b->warp_path) return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
   // RK_PROFILE=1: time every class launch with events and report on stderr
@@ -833,18 +747,11 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
     const int ctas = std::min<int>(rk::kWarpCtasPerSm, (int)((st->smem_optin + 1024) / per_cta));
-    bool no_generic = true;
-    for (auto& hc : b->chunks) no_generic = no_generic && (hc.dev.cls % rk::kNumNck) != 2;
-    const bool warp_ok = ctas >= 12 && !getenv("RK_NO_WARP_PATH");
-    // CTA path: series too long for one-warp CTAs; W warps per CTA so that
-    // the SM holds 24 warps in total
-    const int cta_per_sm = (int)((st->smem_optin + 1024) / (smem + 1024 + sizeof(rk::CtaSlot) * rk::kCtaSlots + 64));
-    const bool cta_ok = !warp_ok && cta_per_sm >= 1 && !getenv("RK_NO_CTA_PATH");
-    if (no_generic && (warp_ok || cta_ok)) {
-      b->warp_path = warp_ok;
-      b->cta_path = !warp_ok;
-      b->warp_ctas_per_sm = warp_ok ? ctas : std::min(cta_per_sm, 6);
-      b->cta_warps = warp_ok ? 1 : std::max(4, std::min(rk::kCtaMaxWarps, rk::kCtaMaxWarps / b->warp_ctas_per_sm));
+    bool ok = ctas >= 12 && !getenv("RK_NO_WARP_PATH");
+    for (auto& hc : b->chunks) ok = ok && (hc.dev.cls % rk::kNumNck) != 2;
+    if (ok) {
+      b->warp_path = true;
+      b->warp_ctas_per_sm = ctas;
       for (int cls = 0; cls < rk::kNumClasses; ++cls) {
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
@@ -887,7 +794,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         }
       }
       if ((int)b->warp_launches.size() > kMaxLaunches) {
-        b->warp_path = b->cta_path = false;
+        b->warp_path = false;
         b->warp_launches.clear();
       }
     }
@@ -962,7 +869,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
-  if (b->warp_path || b->cta_path)
+  if (b->warp_path)
     info->n_launches = (int32_t)b->warp_launches.size();
   else
     for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;

@@ -735,167 +735,3 @@ __global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
 }
 
 }  // namespace rk
-
-// ---------------------------------------------------------------------------
-// CTA path (long or multichannel series that do not fit 24 one-warp CTAs):
-// every warp of the CTA walks the same chunk sequence of the launch (a
-// warp-uniform loop, so the weights stay in uniform registers as in the warp
-// path) over one shared staged series, taking every W-th step of each chunk
-// (rotated per chunk for balance).  Per-warp pools meet in shared-memory
-// slots; the last warp to arrive at a chunk's slot finishes it, so no
-// barrier is needed per chunk (one every kCtaSync chunks bounds how far warps
-// drift apart, which keeps the slot ring safe).
-namespace rk {
-
-constexpr int kCtaMaxWarps = 24;
-constexpr int kCtaSlots = 16;
-constexpr int kCtaSync = 8;
-
-struct CtaSlot {
-  unsigned cnt[4];
-  int ext[4];  // order-preserving keys (fkey) of max (exact) / min (fast)
-  unsigned arrived;
-  unsigned pad_[3];
-};
-
-template <int LEN, int R, int P, int NC, bool EXACT>
-__global__ void __launch_bounds__(32 * kCtaMaxWarps, 1) rocket_cta_kernel(const __grid_constant__ WParams p) {
-  extern __shared__ __align__(16) float smem[];
-  __shared__ CtaSlot slots[kCtaSlots];
-  __shared__ int s_item;
-  asm volatile("griddepcontrol.launch_dependents;");
-  constexpr int G = 2 * P;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int W = blockDim.x >> 5;
-  const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
-  for (int k = tid; k < C * S; k += blockDim.x) {
-    const int t = k % S;
-    if (t < H || t >= H + L) smem[k] = 0.0f;
-  }
-  for (int k = tid; k < kCtaSlots; k += blockDim.x) {
-    for (int g = 0; g < 4; ++g) {
-      slots[k].cnt[g] = 0u;
-      slots[k].ext[g] = fkey(EXACT ? -INFINITY : INFINITY);
-    }
-    slots[k].arrived = 0u;
-  }
-  const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
-  const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
-  const float* sx = smem + H;
-  const float2 one2 = make_float2(p.h.one, p.h.one);
-  unsigned long long done = 0;
-  while (true) {
-    __syncthreads();
-    if (tid == 0) s_item = atomicAdd(p.h.item_counter, 1);
-    __syncthreads();
-    const int item = s_item;
-    if (item >= p.h.n_series) break;
-    stage_rows<EXACT>(smem, p.h.x + (int64_t)item * C * L, C, L, S, H, p.h.vec_in, tid, blockDim.x);
-    __syncthreads();
-    float* orow = p.h.out + (int64_t)item * p.h.ld_out;
-    for (int ci = 0; ci < p.h.n_chunks; ++ci) {
-      if (ci > 0 && ci % kCtaSync == 0) __syncthreads();
-      const WChunk& c = chunks[ci];
-      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
-      float2 w[NC][P][LEN];
-#pragma unroll
-      for (int s = 0; s < NC; ++s)
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-#pragma unroll
-          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
-      const float* chan[NC];
-#pragma unroll
-      for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
-      float thr[G];
-      float2 init[P];
-      chunk_consts<P, EXACT>(c, thr, init);
-      Pool<G> st;
-      pool_init<G, EXACT>(st);
-      // this warp's steps: k = k0, k0 + W, ... of the chunk's step list
-      const int d = c.d, n = c.n, lo = c.lo;
-      const int RD = R * d;
-      const int A = n / RD;
-      const int rem = n - A * RD;
-      const int full_starts = A * d;
-      const int starts = full_starts + min(d, rem);
-      const int nfull = full_starts >> 5;
-      const int nsteps = (starts + 31) >> 5;
-      const int k0 = (warp + ci) % W;
-      const int qW = (32 * W) / d, rW = 32 * W - qW * d;
-      const int dstep = qW * RD + rW;
-      const int i0 = 32 * k0 + lane;
-      int a = (int)((i0 + 0.5f) * c.invd);
-      int s = i0 - a * d;
-      int v0 = a * RD + s;
-      int k = k0;
-      for (; k < nfull; k += W) {
-        chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, true);
-        s += rW;
-        v0 += dstep;
-        if (s >= d) {
-          s -= d;
-          v0 += RD - d;
-        }
-      }
-      for (; k < nsteps; k += W) {
-        const bool live = 32 * k + lane < starts;
-        const int vv = live ? v0 : 0;
-        chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + vv, d, n - vv, L + H - 1, live);
-        s += rW;
-        v0 += dstep;
-        if (s >= d) {
-          s -= d;
-          v0 += RD - d;
-        }
-      }
-      // combine into the chunk's slot; the last warp to arrive finishes it
-      CtaSlot& sl = slots[ci % kCtaSlots];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const unsigned tot = __reduce_add_sync(kFull, st.cnt[g]);
-        const int key = EXACT ? __reduce_max_sync(kFull, fkey(st.ext[g])) : __reduce_min_sync(kFull, fkey(st.ext[g]));
-        if (lane == 0) {
-          atomicAdd(&sl.cnt[g], tot);
-          if (EXACT)
-            atomicMax(&sl.ext[g], key);
-          else
-            atomicMin(&sl.ext[g], key);
-        }
-      }
-      unsigned arrived = 0;
-      if (lane == 0) {
-        __threadfence_block();
-        arrived = atomicAdd(&sl.arrived, 1u);
-      }
-      arrived = __shfl_sync(kFull, arrived, 0);
-      if (arrived == (unsigned)(W - 1)) {
-        __threadfence_block();
-        if (lane < c.nk) {
-          const unsigned cnt = atomicAdd(&sl.cnt[lane], 0u);
-          const float e = fkey_inv(atomicAdd(&sl.ext[lane], 0));
-          const float ppv = __double2float_rn(__ddiv_rn((double)cnt, (double)c.n));
-          const float mx = EXACT ? __fadd_rn(e, c.bias[lane]) : -e;
-          float* dst = orow + (int64_t)c.col[lane] * p.h.fpk;
-          if (p.h.vec_out) {
-            *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
-          } else {
-            dst[0] = ppv;
-            dst[1] = mx;
-          }
-        }
-        __syncwarp();
-        if (lane < 4) {
-          sl.cnt[lane] = 0u;
-          sl.ext[lane] = fkey(EXACT ? -INFINITY : INFINITY);
-        }
-        if (lane == 0) sl.arrived = 0u;
-        __threadfence_block();
-        done += (unsigned long long)c.nk * (unsigned long long)c.n;
-      }
-    }
-  }
-  if (lane == 0 && done) atomicAdd(p.h.executed, done);
-}
-
-}  // namespace rk
