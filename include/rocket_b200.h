@@ -70,7 +70,10 @@ typedef struct rk_bank_info_s {
   int64_t useful_flops_per_series; /* sum_k 2*in-range taps + l_out_k */
   int64_t device_bytes; /* device memory held by the bank */
   int32_t device;
-  int32_t n_launches;   /* kernel launches per transform (non-empty classes) */
+  int32_t n_launches;   /* kernel launches per float32 transform */
+  int32_t path;         /* 1: one-warp CTAs with parameter-block weights
+                           (short series), 0: 16-warp class CTAs */
+  int32_t ctas_per_sm;  /* resident CTAs per SM on the warp path */
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

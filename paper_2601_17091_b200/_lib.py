@@ -67,6 +67,8 @@ class BankInfo(ctypes.Structure):
         ("device_bytes", ctypes.c_int64),
         ("device", ctypes.c_int32),
         ("n_launches", ctypes.c_int32),
+        ("path", ctypes.c_int32),
+        ("ctas_per_sm", ctypes.c_int32),
     ]
 
 

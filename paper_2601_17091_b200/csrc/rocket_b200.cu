@@ -289,12 +289,12 @@ void release_worker(DeviceState* st, Worker* w) {
   st->free_workers.push_back(w);
 }
 
-int set_kernel_smem(DeviceState* st, KernelFn fn, int bytes) {
+int set_kernel_smem(DeviceState* st, const void* fn, int bytes) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
-  auto it = st->attr_smem.find((const void*)fn);
+  auto it = st->attr_smem.find(fn);
   if (it == st->attr_smem.end() || it->second < bytes) {
-    RK_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    st->attr_smem[(const void*)fn] = bytes;
+    RK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    st->attr_smem[fn] = bytes;
   }
   return RK_OK;
 }
@@ -320,9 +320,7 @@ int exec_cls(int cls, int exact) {
 
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
-// Enqueue the transform of n series already on the device: one launch per
-// non-empty chunk class, all on `stream`.
-// Warp path: one PDL-chained launch per parameter block.
+// Warp path: one PDL-chained launch per parameter block, all on `stream`.
 int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
                 int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
@@ -337,7 +335,7 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     const auto& wl = b->warp_launches[li];
     WarpFn fn = kernel_table().wfn[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
-    int rc = set_kernel_smem(st, (KernelFn)fn, smem);
+    int rc = set_kernel_smem(st, (const void*)fn, smem);
     if (rc) return rc;
     const int nck = wl.cls % rk::kNumNck;
     const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
@@ -457,7 +455,7 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
     const int want = (4 * rk::kThreads / 32 + nchunks - 1) / nchunks;
     while (spi < want && spi < 16 && (int64_t)(spi + 1) * series_bytes <= smem_cap / 2 && spi < n) ++spi;
     const int smem = spi * series_bytes;
-    int rc0 = set_kernel_smem(st, fn, smem);
+    int rc0 = set_kernel_smem(st, (const void*)fn, smem);
     if (rc0) return rc0;
     int ctas_per_sm = 1;
     RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, (const void*)fn, rk::kThreads, smem));
@@ -608,6 +606,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     groups[key].push_back(k);
   }
   if (halo > (1 << 24)) return fail(RK_ERR_CAPACITY, "padding %d too large", halo);
+  halo = (halo + 3) / 4 * 4;  // keep staged rows 16-byte aligned (float4 staging)
 
   DeviceState* st = nullptr;
   int rc = device_state(device, &st);
@@ -869,6 +868,8 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
+  info->path = b->warp_path ? 1 : 0;
+  info->ctas_per_sm = b->warp_ctas_per_sm;
   if (b->warp_path)
     info->n_launches = (int32_t)b->warp_launches.size();
   else
