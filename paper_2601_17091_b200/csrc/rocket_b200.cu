@@ -467,8 +467,6 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
     int* d_bs = nullptr;
     int rc = b->blocks_for(cls, nb, &d_bs);
     if (rc) return rc;
-    rc = set_kernel_smem(st, fn, smem);
-    if (rc) return rc;
     rk::LaunchArgs a;
     a.x = d_x;
     a.out = d_out;
