@@ -106,7 +106,9 @@ struct rk_bank_s {
     std::vector<rk::float4_t> blob;
   };
   bool warp_path = false;  // one-warp CTAs, parameter-block launches
+  bool wide_path = false;  // same launches, W warps share one staged series
   int warp_ctas_per_sm = 0;
+  int wide_warps = 1;
   std::vector<WarpLaunch> warp_launches;
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
@@ -235,10 +237,11 @@ using rk::WarpFn;
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
   WarpFn wfn[2 * rk::kNumClasses] = {};
+  WarpFn dfn[2 * rk::kNumClasses] = {};
   KernelTable() {
-    rk_fill_tables_7(fn, wfn);
-    rk_fill_tables_9(fn, wfn);
-    rk_fill_tables_11(fn, wfn);
+    rk_fill_tables_7(fn, wfn, dfn);
+    rk_fill_tables_9(fn, wfn, dfn);
+    rk_fill_tables_11(fn, wfn, dfn);
   }
 };
 const KernelTable& kernel_table() {
@@ -333,7 +336,8 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->warp_launches.size(); ++li) {
     const auto& wl = b->warp_launches[li];
-    WarpFn fn = kernel_table().wfn[2 * exec_cls(wl.cls, exact) + exact];
+    const WarpFn* tab = b->wide_path ? kernel_table().dfn : kernel_table().wfn;
+    WarpFn fn = tab[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (const void*)fn, smem);
     if (rc) return rc;
@@ -360,7 +364,7 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(32);
+    cfg.blockDim = dim3(32 * b->wide_warps);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -435,7 +439,8 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
-  if (b->warp_path) return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
+  if (b->warp_path || b->wide_path)
+    return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
   // RK_PROFILE=1: time every class launch with events and report on stderr
@@ -744,11 +749,16 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
     const int ctas = std::min<int>(rk::kWarpCtasPerSm, (int)((st->smem_optin + 1024) / per_cta));
-    bool ok = ctas >= 12 && !getenv("RK_NO_WARP_PATH");
-    for (auto& hc : b->chunks) ok = ok && (hc.dev.cls % rk::kNumNck) != 2;
-    if (ok) {
-      b->warp_path = true;
-      b->warp_ctas_per_sm = ctas;
+    bool no_generic = true;
+    for (auto& hc : b->chunks) no_generic = no_generic && (hc.dev.cls % rk::kNumNck) != 2;
+    const bool warp_ok = no_generic && ctas >= 12 && !getenv("RK_NO_WARP_PATH");
+    // wide path: fewer CTAs per SM, each with enough warps for 24 per SM
+    const bool wide_ok = no_generic && !warp_ok && ctas >= 1 && !getenv("RK_NO_WIDE_PATH");
+    if (warp_ok || wide_ok) {
+      b->warp_path = warp_ok;
+      b->wide_path = wide_ok;
+      b->warp_ctas_per_sm = warp_ok ? ctas : std::min(ctas, 6);
+      b->wide_warps = warp_ok ? 1 : std::max(4, rk::kWideMaxWarps / b->warp_ctas_per_sm);
       for (int cls = 0; cls < rk::kNumClasses; ++cls) {
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
@@ -791,7 +801,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         }
       }
       if ((int)b->warp_launches.size() > kMaxLaunches) {
-        b->warp_path = false;
+        b->warp_path = b->wide_path = false;
         b->warp_launches.clear();
       }
     }
@@ -866,9 +876,9 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
-  info->path = b->warp_path ? 1 : 0;
+  info->path = b->warp_path ? 1 : (b->wide_path ? 2 : 0);
   info->ctas_per_sm = b->warp_ctas_per_sm;
-  if (b->warp_path)
+  if (b->warp_path || b->wide_path)
     info->n_launches = (int32_t)b->warp_launches.size();
   else
     for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;

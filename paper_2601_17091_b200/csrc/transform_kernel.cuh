@@ -735,3 +735,79 @@ __global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
 }
 
 }  // namespace rk
+
+// ---------------------------------------------------------------------------
+// Wide path (series too long for one-warp CTAs, e.g. L = 16384 or three
+// 2048-long channels): W warps per CTA share one staged series and claim
+// whole chunks of the launch's parameter block from a shared counter.  The
+// claimed index is passed through a warp REDUX, whose result lives in a
+// uniform register, so — as on the warp path — ptxas loads the chunk's
+// descriptor and weights with LDCU into uniform registers and FFMA2 reads
+// the weights as UR operands.
+namespace rk {
+
+constexpr int kWideMaxWarps = 24;
+
+template <int LEN, int R, int P, int NC, bool EXACT>
+__global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int s_item;
+  __shared__ int s_next;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
+  for (int k = tid; k < C * S; k += blockDim.x) {
+    const int t = k % S;
+    if (t < H || t >= H + L) smem[k] = 0.0f;
+  }
+  const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
+  const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
+  const float* sx = smem + H;
+  const float2 one2 = make_float2(p.h.one, p.h.one);
+  unsigned long long done = 0;
+  while (true) {
+    __syncthreads();  // every warp has left the previous series
+    if (tid == 0) {
+      s_item = atomicAdd(p.h.item_counter, 1);
+      s_next = 0;
+    }
+    __syncthreads();
+    const int item = s_item;
+    if (item >= p.h.n_series) break;
+    stage_rows<EXACT>(smem, p.h.x + (int64_t)item * C * L, C, L, S, H, p.h.vec_in, tid, blockDim.x);
+    __syncthreads();
+    float* orow = p.h.out + (int64_t)item * p.h.ld_out;
+    while (true) {
+      int ci = 0;
+      if (lane == 0) ci = atomicAdd(&s_next, 1);
+      // REDUX result lands in a uniform register: the chunk index is
+      // warp-uniform for ptxas from here on
+      ci = __reduce_max_sync(kFull, __shfl_sync(kFull, ci, 0));
+      if (ci >= p.h.n_chunks) break;
+      const WChunk& c = chunks[ci];
+      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
+      float2 w[NC][P][LEN];
+#pragma unroll
+      for (int s = 0; s < NC; ++s)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
+      const float* chan[NC];
+#pragma unroll
+      for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+      float thr[2 * P];
+      float2 init[P];
+      chunk_consts<P, EXACT>(c, thr, init);
+      Pool<2 * P> st;
+      pool_init<2 * P, EXACT>(st);
+      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
+                                          L + H - 1, lane);
+      finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
+      done += (unsigned long long)c.nk * (unsigned long long)c.n;
+    }
+  }
+  if (lane == 0 && done) atomicAdd(p.h.executed, done);
+}
+
+}  // namespace rk
