@@ -341,7 +341,7 @@ def main():
                          "flops_per_series": flops_series,
                          "peak_source": "measured FFMA2 microbenchmark (profiles/r01_fp32_peak_microbench.jsonl); "
                                         "MEASURED_PEAKS.json has no FP32 entry",
-                         "kernel": {1: "rocket_warp_kernel", 2: "rocket_wide_kernel"}.get(info["path"], "rocket_class_kernel")
+                         "kernel": ("rocket_wide_kernel" if info["path"] == 1 else "rocket_class_kernel")
                                    + f" x {info['n_launches']} launches (one transform; DESIGN.md §4)"},
             "other_mode": {"mode": other, "ms_per_step": ms_other / args.steps,
                            "value": total_series / (ms_other / 1e3),
@@ -352,7 +352,7 @@ def main():
             "energy": energy,
             "gpu_launches": int(info["n_launches"]) * args.steps,
             "bank": {"groups": info["n_groups"], "chunks": info["n_chunks"], "launches_per_step": info["n_launches"],
-                     "smem_bytes": info["smem_bytes"], "path": {1: "warp", 2: "wide"}.get(info["path"], "class"),
+                     "smem_bytes": info["smem_bytes"], "path": ("wide" if info["path"] == 1 else "class"),
                      "ctas_per_sm": info["ctas_per_sm"]},
         }
         print(json.dumps(line), flush=True)

@@ -71,10 +71,10 @@ typedef struct rk_bank_info_s {
   int64_t device_bytes; /* device memory held by the bank */
   int32_t device;
   int32_t n_launches;   /* kernel launches per float32 transform */
-  int32_t path;         /* 1: one-warp CTAs, parameter-block weights (short
-                           series); 2: wide CTAs sharing a series, same
-                           weights; 0: class CTAs (>= 3 channel slots) */
-  int32_t ctas_per_sm;  /* resident CTAs per SM on paths 1 and 2 */
+  int32_t path;         /* 1: wide kernel (parameter-block weights in
+                           uniform registers); 0: class kernel (banks with
+                           >= 3-channel kernels) */
+  int32_t ctas_per_sm;  /* resident CTAs per SM on the wide path */
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

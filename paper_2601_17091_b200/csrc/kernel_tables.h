@@ -12,8 +12,7 @@ using WarpFn = void (*)(const WParams);
 }  // namespace rk
 
 // Fill the (class, mode) slots of length LEN: class kernels into cls_tab,
-// warp-path kernels into warp_tab, wide-path kernels into wide_tab (index
-// 2 * cls + exact).
-void rk_fill_tables_7(rk::KernelFn* cls_tab, rk::WarpFn* warp_tab, rk::WarpFn* wide_tab);
-void rk_fill_tables_9(rk::KernelFn* cls_tab, rk::WarpFn* warp_tab, rk::WarpFn* wide_tab);
-void rk_fill_tables_11(rk::KernelFn* cls_tab, rk::WarpFn* warp_tab, rk::WarpFn* wide_tab);
+// wide kernels into wide_tab (index 2 * cls + exact).
+void rk_fill_tables_7(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab);
+void rk_fill_tables_9(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab);
+void rk_fill_tables_11(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab);

@@ -16,34 +16,32 @@ void fill_class(rk::KernelFn* t, int cls) {
 }
 
 template <int R, int P, int NC>
-void fill_warp(rk::WarpFn* t, rk::WarpFn* wide, int cls) {
-  t[2 * cls + 0] = rk::rocket_warp_kernel<RK_LEN, R, P, NC, false>;
-  t[2 * cls + 1] = rk::rocket_warp_kernel<RK_LEN, R, P, NC, true>;
+void fill_wide(rk::WarpFn* wide, int cls) {
   wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false>;
   wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
 }
 
 template <int RI>
-void fill_r(rk::KernelFn* ct, rk::WarpFn* wt, rk::WarpFn* dt) {
+void fill_r(rk::KernelFn* ct, rk::WarpFn* dt) {
   constexpr int R = rk::r_of(RI);
   const int base = (kLenIdx * rk::kNumR + RI) * rk::kNumNck;
   fill_class<R, 0>(ct, base + 0);
   fill_class<R, 1>(ct, base + 1);
   fill_class<R, 3>(ct, base + 3);
   if constexpr (R == 1) fill_class<R, 2>(ct, base + 2);  // generic channels: 1 position per lane
-  fill_warp<R, 2, 1>(wt, dt, base + 0);
-  fill_warp<R, 1, 2>(wt, dt, base + 1);
-  fill_warp<R, 1, 1>(wt, dt, base + 3);
+  fill_wide<R, 2, 1>(dt, base + 0);
+  fill_wide<R, 1, 2>(dt, base + 1);
+  fill_wide<R, 1, 1>(dt, base + 3);
 }
 }  // namespace
 
 #define RK_CAT2(a, b) a##b
 #define RK_CAT(a, b) RK_CAT2(a, b)
 
-void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* wt, rk::WarpFn* dt) {
-  fill_r<0>(ct, wt, dt);
-  fill_r<1>(ct, wt, dt);
-  fill_r<2>(ct, wt, dt);
-  fill_r<3>(ct, wt, dt);
-  fill_r<4>(ct, wt, dt);
+void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt) {
+  fill_r<0>(ct, dt);
+  fill_r<1>(ct, dt);
+  fill_r<2>(ct, dt);
+  fill_r<3>(ct, dt);
+  fill_r<4>(ct, dt);
 }

@@ -98,18 +98,17 @@ struct rk_bank_s {
   std::vector<int64_t> cost_prefix;
   int cls_begin[rk::kNumClasses] = {};
   int cls_end[rk::kNumClasses] = {};
-  // warp path (short series): per-launch parameter blocks, built once
-  struct WarpLaunch {
+  // wide path: per-launch parameter blocks, built once
+  struct WideLaunch {
     int cls;
     int n_chunks;
     int64_t dense_flops;  // 2 * taps * positions of one series (diagnostics)
     std::vector<rk::float4_t> blob;
   };
-  bool warp_path = false;  // one-warp CTAs, parameter-block launches
-  bool wide_path = false;  // same launches, W warps share one staged series
-  int warp_ctas_per_sm = 0;
+  bool wide_path = false;  // parameter-block launches, W warps share a series
+  int wide_ctas_per_sm = 0;
   int wide_warps = 1;
-  std::vector<WarpLaunch> warp_launches;
+  std::vector<WideLaunch> wide_launches;
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
   int* d_chan_off = nullptr;
@@ -236,12 +235,11 @@ using rk::KernelFn;
 using rk::WarpFn;
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
-  WarpFn wfn[2 * rk::kNumClasses] = {};
   WarpFn dfn[2 * rk::kNumClasses] = {};
   KernelTable() {
-    rk_fill_tables_7(fn, wfn, dfn);
-    rk_fill_tables_9(fn, wfn, dfn);
-    rk_fill_tables_11(fn, wfn, dfn);
+    rk_fill_tables_7(fn, dfn);
+    rk_fill_tables_9(fn, dfn);
+    rk_fill_tables_11(fn, dfn);
   }
 };
 const KernelTable& kernel_table() {
@@ -323,8 +321,8 @@ int exec_cls(int cls, int exact) {
 
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
-// Warp path: one PDL-chained launch per parameter block, all on `stream`.
-int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
+// Wide path: one PDL-chained launch per parameter block, all on `stream`.
+int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
                 int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   static const bool profile = getenv("RK_PROFILE") != nullptr;
@@ -332,13 +330,12 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   static std::mutex params_mu;
   std::lock_guard<std::mutex> lk(params_mu);
   const int smem = b->smem_bytes;
-  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * b->warp_ctas_per_sm);
+  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * b->wide_ctas_per_sm);
   std::vector<cudaEvent_t> evs;
-  for (size_t li = 0; li < b->warp_launches.size(); ++li) {
-    const auto& wl = b->warp_launches[li];
-    const WarpFn* tab = b->wide_path ? kernel_table().dfn : kernel_table().wfn;
-    WarpFn fn = tab[2 * exec_cls(wl.cls, exact) + exact];
-    if (!fn) return fail(RK_ERR_UNSUPPORTED, "no warp kernel for class %d", wl.cls);
+  for (size_t li = 0; li < b->wide_launches.size(); ++li) {
+    const auto& wl = b->wide_launches[li];
+    WarpFn fn = kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
+    if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (const void*)fn, smem);
     if (rc) return rc;
     const int nck = wl.cls % rk::kNumNck;
@@ -391,8 +388,8 @@ int launch_warp(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     for (size_t i = 0; i + 1 < evs.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
-      const auto& wl = b->warp_launches[i];
-      fprintf(stderr, "RK_PROFILE warp len=%d R=%d nck=%d exact=%d chunks=%d grid=%lld ms=%.3f dense_tflops=%.2f\n",
+      const auto& wl = b->wide_launches[i];
+      fprintf(stderr, "RK_PROFILE wide len=%d R=%d nck=%d exact=%d chunks=%d grid=%lld ms=%.3f dense_tflops=%.2f\n",
               c_len(wl.cls), rk::r_of((wl.cls / rk::kNumNck) % rk::kNumR), wl.cls % rk::kNumNck, exact,
               wl.n_chunks, (long long)grid, ms, wl.dense_flops * (double)n / (ms * 1e-3) / 1e12);
     }
@@ -439,8 +436,7 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
-  if (b->warp_path || b->wide_path)
-    return launch_warp(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
+  if (b->wide_path) return launch_wide(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters);
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   const int series_bytes = b->smem_bytes;
   // RK_PROFILE=1: time every class launch with events and report on stderr
@@ -744,21 +740,19 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   b->cost_prefix.assign(b->chunks.size() + 1, 0);
   for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
 
-  // Warp path: every chunk has <= 2 channel slots and 24 one-warp CTAs
-  // (each with its own staged series) fit in an SM's shared memory.
+  // Wide path: every chunk has <= 2 channel slots.  CTAs per SM as shared
+  // memory allows (at most 8, measured best for L = 1024..2048), warps per
+  // CTA so the SM holds 24 warps (the ~80-register budget).
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
-    const int ctas = std::min<int>(rk::kWarpCtasPerSm, (int)((st->smem_optin + 1024) / per_cta));
+    const int by_smem = (int)((st->smem_optin + 1024) / per_cta);
     bool no_generic = true;
     for (auto& hc : b->chunks) no_generic = no_generic && (hc.dev.cls % rk::kNumNck) != 2;
-    const bool warp_ok = no_generic && ctas >= 12 && !getenv("RK_NO_WARP_PATH");
-    // wide path: fewer CTAs per SM, each with enough warps for 24 per SM
-    const bool wide_ok = no_generic && !warp_ok && ctas >= 1 && !getenv("RK_NO_WIDE_PATH");
-    if (warp_ok || wide_ok) {
-      b->warp_path = warp_ok;
-      b->wide_path = wide_ok;
-      b->warp_ctas_per_sm = warp_ok ? ctas : std::min(ctas, 6);
-      b->wide_warps = warp_ok ? 1 : std::max(4, rk::kWideMaxWarps / b->warp_ctas_per_sm);
+    const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 8;
+    if (no_generic && by_smem >= 1 && !getenv("RK_NO_WIDE_PATH")) {
+      b->wide_path = true;
+      b->wide_ctas_per_sm = std::min(by_smem, cap);
+      b->wide_warps = std::max(1, rk::kWideMaxWarps / b->wide_ctas_per_sm);
       for (int cls = 0; cls < rk::kNumClasses; ++cls) {
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
@@ -770,7 +764,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         const int cap = (rk::kBlobFloat4 * 16) / per_chunk;
         for (int i0 = cb; i0 < ce; i0 += cap) {
           const int nch = std::min(cap, ce - i0);
-          rk_bank_s::WarpLaunch wl;
+          rk_bank_s::WideLaunch wl;
           wl.cls = cls;
           wl.n_chunks = nch;
           wl.dense_flops = 0;
@@ -797,12 +791,12 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
             std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
             wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
           }
-          b->warp_launches.push_back(std::move(wl));
+          b->wide_launches.push_back(std::move(wl));
         }
       }
-      if ((int)b->warp_launches.size() > kMaxLaunches) {
-        b->warp_path = b->wide_path = false;
-        b->warp_launches.clear();
+      if ((int)b->wide_launches.size() > kMaxLaunches) {
+        b->wide_path = false;
+        b->wide_launches.clear();
       }
     }
   }
@@ -876,10 +870,10 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
-  info->path = b->warp_path ? 1 : (b->wide_path ? 2 : 0);
-  info->ctas_per_sm = b->warp_ctas_per_sm;
-  if (b->warp_path || b->wide_path)
-    info->n_launches = (int32_t)b->warp_launches.size();
+  info->path = b->wide_path ? 1 : 0;
+  info->ctas_per_sm = b->wide_ctas_per_sm;
+  if (b->wide_path)
+    info->n_launches = (int32_t)b->wide_launches.size();
   else
     for (int c = 0; c < rk::kNumClasses; ++c) info->n_launches += b->cls_end[c] > b->cls_begin[c] ? 1 : 0;
   return RK_OK;

@@ -15,11 +15,12 @@
 //   * kernel pairs are packed into FFMA2 (sm_100 packed FP32) with the
 //     series value as the scalar-broadcast operand.
 // Two kernels drive it:
-//   * rocket_warp_kernel  (series that fit 24 one-warp CTAs per SM): chunk
+//   * rocket_wide_kernel  (chunks with <= 2 channel slots): chunk
 //     descriptors and weights travel in the __grid_constant__ parameter
 //     block, so the weights sit in uniform registers (FFMA2 UR operands);
-//   * rocket_class_kernel (long / many-channel series): 8-warp CTAs share
-//     one staged series, weights come from global memory.
+//     W warps per CTA share one staged series;
+//   * rocket_class_kernel (banks with >= 3-channel kernels): 16-warp CTAs
+//     share one staged series, weights come from global memory.
 //
 // Arithmetic (both modes are deterministic run to run):
 //   EXACT: acc = RN(acc + RN(w*x)) tap by tap from the first product
@@ -534,14 +535,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
 }
 
 // ---------------------------------------------------------------------------
-// Warp path (short series): one warp per CTA, 24 CTAs per SM.  The chunk
-// descriptors and weights of one launch travel in the kernel's
-// __grid_constant__ parameter block (<= 32 KB); the chunk loop counter is
-// warp-uniform, so ptxas keeps the weights in uniform registers (LDCU) and
-// FFMA2 reads them as UR operands — ~70 vector registers instead of ~120,
-// hence 1.5x the resident warps of the class kernel.  Each CTA stages its
-// own copy of the series (C * sstride floats) and claims series dynamically.
-constexpr int kWarpCtasPerSm = 24;
+// Parameter-block launches (rocket_wide_kernel): the chunk descriptors and
+// weights of one launch travel in the kernel's __grid_constant__ parameter
+// block (<= 32 KB), so a warp-uniform chunk index lets ptxas keep the
+// weights in uniform registers (LDCU) and FFMA2 read them as UR operands —
+// ~80 vector registers instead of ~120, hence 24 resident warps per SM.
 constexpr int kParamBytes = 32000;
 struct float4_t {  // host-side storage of the parameter blob
   float x, y, z, w;
@@ -582,59 +580,6 @@ struct WParams {
   WHeader h;
   float4 blob[kBlobFloat4];  // n_chunks WChunk, then n_chunks weight blocks
 };
-
-template <int LEN, int R, int P, int NC, bool EXACT>
-__global__ void __launch_bounds__(32, kWarpCtasPerSm) rocket_warp_kernel(const __grid_constant__ WParams p) {
-  extern __shared__ __align__(16) float smem[];
-  // the next class launch (PDL) may start filling SMs as this one drains;
-  // launches of one transform are independent (disjoint output columns)
-  asm volatile("griddepcontrol.launch_dependents;");
-  const int lane = threadIdx.x;
-  const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
-  for (int k = lane; k < C * S; k += 32) {
-    const int t = k % S;
-    if (t < H || t >= H + L) smem[k] = 0.0f;
-  }
-  const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
-  const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
-  const float* sx = smem + H;
-  const float2 one2 = make_float2(p.h.one, p.h.one);
-  unsigned long long done = 0;
-  while (true) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(p.h.item_counter, 1);
-    item = __shfl_sync(kFull, item, 0);
-    if (item >= p.h.n_series) break;
-    __syncwarp();
-    stage_rows<EXACT>(smem, p.h.x + (int64_t)item * C * L, C, L, S, H, p.h.vec_in, lane, 32);
-    __syncwarp();
-    float* orow = p.h.out + (int64_t)item * p.h.ld_out;
-    for (int ci = 0; ci < p.h.n_chunks; ++ci) {
-      const WChunk& c = chunks[ci];
-      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
-      float2 w[NC][P][LEN];
-#pragma unroll
-      for (int s = 0; s < NC; ++s)
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-#pragma unroll
-          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
-      const float* chan[NC];
-#pragma unroll
-      for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
-      float thr[2 * P];
-      float2 init[P];
-      chunk_consts<P, EXACT>(c, thr, init);
-      Pool<2 * P> st;
-      pool_init<2 * P, EXACT>(st);
-      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
-                                          L + H - 1, lane);
-      finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
-      done += (unsigned long long)c.nk * (unsigned long long)c.n;
-    }
-  }
-  if (lane == 0 && done) atomicAdd(p.h.executed, done);
-}
 
 }  // namespace rk
 
@@ -737,13 +682,13 @@ __global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
 }  // namespace rk
 
 // ---------------------------------------------------------------------------
-// Wide path (series too long for one-warp CTAs, e.g. L = 16384 or three
-// 2048-long channels): W warps per CTA share one staged series and claim
-// whole chunks of the launch's parameter block from a shared counter.  The
-// claimed index is passed through a warp REDUX, whose result lives in a
-// uniform register, so — as on the warp path — ptxas loads the chunk's
-// descriptor and weights with LDCU into uniform registers and FFMA2 reads
-// the weights as UR operands.
+// Wide kernel (every chunk class with <= 2 channel slots): W warps per CTA
+// share one staged series and claim whole chunks of the launch's parameter
+// block from a shared counter; CTAs claim series from a global counter.  The
+// claimed chunk index is passed through a warp REDUX, whose result lives in
+// a uniform register, so ptxas loads the chunk's descriptor and weights with
+// LDCU into uniform registers and FFMA2 reads the weights as UR operands.
+// CTAs x W is sized for 24 warps per SM (shared memory permitting).
 namespace rk {
 
 constexpr int kWideMaxWarps = 24;
