@@ -106,8 +106,8 @@ struct rk_bank_s {
     std::vector<rk::float4_t> blob;
   };
   bool wide_path = false;  // parameter-block launches, W warps share a series
-  int wide_ctas_per_sm = 0;
-  int wide_warps = 1;
+  int wide_ctas_per_sm = 0;  // default CTAs per SM (many series)
+  int wide_ctas_smem = 0;    // shared-memory limit of CTAs per SM
   std::vector<WideLaunch> wide_launches;
   rk::DevChunk* d_chunks = nullptr;
   float* d_weights = nullptr;
@@ -330,7 +330,12 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   static std::mutex params_mu;
   std::lock_guard<std::mutex> lk(params_mu);
   const int smem = b->smem_bytes;
-  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * b->wide_ctas_per_sm);
+  // Few series: more, narrower CTAs (down to one warp) so every SM still has
+  // work; many series: wide_ctas_per_sm CTAs of 24/ctas warps.
+  int ctas = b->wide_ctas_per_sm;
+  if (n < 4LL * st->sms * ctas) ctas = std::min(b->wide_ctas_smem, rk::kWideMaxWarps);
+  const int warps = std::max(1, rk::kWideMaxWarps / ctas);
+  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
@@ -361,7 +366,7 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(32 * b->wide_warps);
+    cfg.blockDim = dim3(32 * warps);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -751,8 +756,8 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 8;
     if (no_generic && by_smem >= 1 && !getenv("RK_NO_WIDE_PATH")) {
       b->wide_path = true;
+      b->wide_ctas_smem = by_smem;
       b->wide_ctas_per_sm = std::min(by_smem, cap);
-      b->wide_warps = std::max(1, rk::kWideMaxWarps / b->wide_ctas_per_sm);
       for (int cls = 0; cls < rk::kNumClasses; ++cls) {
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
