@@ -335,13 +335,20 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   int ctas = b->wide_ctas_per_sm;
   if (n < 4LL * st->sms * ctas) ctas = std::min(b->wide_ctas_smem, rk::kWideMaxWarps);
   const int warps = std::max(1, rk::kWideMaxWarps / ctas);
-  const int64_t grid = std::min<int64_t>(n, (int64_t)st->sms * ctas);
+  // two series per item when they fit at the same CTA count: the chunk's
+  // weights and setup serve both
+  const int spi_env = getenv("RK_SPI") ? atoi(getenv("RK_SPI")) : 2;
+  int spi = 1;
+  if (spi_env >= 2 && n >= 8LL * st->sms * ctas &&
+      (int64_t)ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
+    spi = 2;
+  const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
     WarpFn fn = kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
-    int rc = set_kernel_smem(st, (const void*)fn, smem);
+    int rc = set_kernel_smem(st, (const void*)fn, smem * spi);
     if (rc) return rc;
     const int nck = wl.cls % rk::kNumNck;
     const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
@@ -363,11 +370,12 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     h.vec_in = ((b->L % 4) == 0 && ((uintptr_t)d_x % 16) == 0 && (b->sstride % 4) == 0 && (b->halo % 4) == 0) ? 1 : 0;
     h.one = 1.0f;
     h.wbytes = NC * P * len * 8;
+    h.spi = spi;
     std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(32 * warps);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = smem * spi;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

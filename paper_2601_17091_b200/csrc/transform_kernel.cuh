@@ -574,6 +574,7 @@ struct WHeader {
   int vec_in;
   float one;
   int wbytes;  // bytes of weights per chunk
+  int spi;     // series staged per CTA item (wide kernel: 1 or 2)
 };
 constexpr int kBlobFloat4 = (kParamBytes - (int)sizeof(WHeader)) / 16;
 struct WParams {
@@ -701,27 +702,28 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
   asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, lane = tid & 31;
   const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
-  for (int k = tid; k < C * S; k += blockDim.x) {
-    const int t = k % S;
+  const int SPI = p.h.spi;
+  const int slot = C * S;
+  for (int k = tid; k < SPI * slot; k += blockDim.x) {
+    const int t = (k % slot) % S;
     if (t < H || t >= H + L) smem[k] = 0.0f;
   }
   const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
   const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
-  const float* sx = smem + H;
   const float2 one2 = make_float2(p.h.one, p.h.one);
   unsigned long long done = 0;
   while (true) {
-    __syncthreads();  // every warp has left the previous series
+    __syncthreads();  // every warp has left the previous item
     if (tid == 0) {
       s_item = atomicAdd(p.h.item_counter, 1);
       s_next = 0;
     }
     __syncthreads();
-    const int item = s_item;
-    if (item >= p.h.n_series) break;
-    stage_rows<EXACT>(smem, p.h.x + (int64_t)item * C * L, C, L, S, H, p.h.vec_in, tid, blockDim.x);
+    const int64_t series0 = (int64_t)s_item * SPI;
+    if (series0 >= p.h.n_series) break;
+    const int ns = (int)min<int64_t>(SPI, p.h.n_series - series0);
+    stage_rows<EXACT>(smem, p.h.x + series0 * C * L, ns * C, L, S, H, p.h.vec_in, tid, blockDim.x);
     __syncthreads();
-    float* orow = p.h.out + (int64_t)item * p.h.ld_out;
     while (true) {
       int ci = 0;
       if (lane == 0) ci = atomicAdd(&s_next, 1);
@@ -738,18 +740,22 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         for (int q = 0; q < P; ++q)
 #pragma unroll
           for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
-      const float* chan[NC];
-#pragma unroll
-      for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
       float thr[2 * P];
       float2 init[P];
       chunk_consts<P, EXACT>(c, thr, init);
-      Pool<2 * P> st;
-      pool_init<2 * P, EXACT>(st);
-      run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
-                                          L + H - 1, lane);
-      finish_chunk<2 * P, EXACT>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
-      done += (unsigned long long)c.nk * (unsigned long long)c.n;
+      // the chunk's weights serve every staged series of the item
+      for (int si = 0; si < ns; ++si) {
+        const float* sx = smem + si * slot + H;
+        const float* chan[NC];
+#pragma unroll
+        for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+        Pool<2 * P> st;
+        pool_init<2 * P, EXACT>(st);
+        run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
+                                            L + H - 1, lane);
+        finish_chunk<2 * P, EXACT>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out, lane);
+        done += (unsigned long long)c.nk * (unsigned long long)c.n;
+      }
     }
   }
   if (lane == 0 && done) atomicAdd(p.h.executed, done);
