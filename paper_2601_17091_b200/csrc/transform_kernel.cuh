@@ -721,7 +721,8 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
     __syncthreads();
     const int64_t series0 = (int64_t)s_item * SPI;
     if (series0 >= p.h.n_series) break;
-    const int ns = (int)min<int64_t>(SPI, p.h.n_series - series0);
+    const int64_t left = p.h.n_series - series0;
+    const int ns = left < SPI ? (int)left : SPI;
     stage_rows<EXACT>(smem, p.h.x + series0 * C * L, ns * C, L, S, H, p.h.vec_in, tid, blockDim.x);
     __syncthreads();
     while (true) {
