@@ -335,13 +335,13 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   int ctas = b->wide_ctas_per_sm;
   if (n < 4LL * st->sms * ctas) ctas = std::min(b->wide_ctas_smem, rk::kWideMaxWarps);
   const int warps = std::max(1, rk::kWideMaxWarps / ctas);
-  // two series per item when they fit at the same CTA count: the chunk's
-  // weights and setup serve both
-  const int spi_env = getenv("RK_SPI") ? atoi(getenv("RK_SPI")) : 2;
+  // several series per item when they fit at the same CTA count: each
+  // chunk's weights and setup serve all of them
+  const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 4;
   int spi = 1;
-  if (spi_env >= 2 && n >= 8LL * st->sms * ctas &&
-      (int64_t)ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
-    spi = 2;
+  while (spi < spi_max && n >= 8LL * (spi + 1) * st->sms * ctas &&
+         (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
+    ++spi;
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
