@@ -337,7 +337,7 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   const int warps = std::max(1, rk::kWideMaxWarps / ctas);
   // several series per item when they fit at the same CTA count: each
   // chunk's weights and setup serve all of them
-  const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 4;
+  const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 8;
   int spi = 1;
   while (spi < spi_max && n >= 8LL * (spi + 1) * st->sms * ctas &&
          (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
