@@ -754,14 +754,15 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
 
   // Wide path: every chunk has <= 2 channel slots.  CTAs per SM as shared
-  // memory allows (at most 8, measured best for L = 1024..2048), warps per
-  // CTA so the SM holds 24 warps (the ~80-register budget).
+  // memory allows (at most 6: 6 x 4 warps with up to 4 series per item
+  // measured best at L = 1024), warps per CTA so the SM holds 24 warps (the
+  // ~80-register budget).
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
     const int by_smem = (int)((st->smem_optin + 1024) / per_cta);
     bool no_generic = true;
     for (auto& hc : b->chunks) no_generic = no_generic && (hc.dev.cls % rk::kNumNck) != 2;
-    const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 8;
+    const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6;
     if (no_generic && by_smem >= 1 && !getenv("RK_NO_WIDE_PATH")) {
       b->wide_path = true;
       b->wide_ctas_smem = by_smem;
