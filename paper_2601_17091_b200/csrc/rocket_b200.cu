@@ -339,7 +339,8 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   // chunk's weights and setup serve all of them
   const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 8;
   int spi = 1;
-  while (spi < spi_max && n >= 8LL * (spi + 1) * st->sms * ctas &&
+  const int64_t min_items = getenv("RK_MIN_ITEMS") ? atoi(getenv("RK_MIN_ITEMS")) : 8;
+  while (spi < spi_max && n >= min_items * (spi + 1) * st->sms * ctas &&
          (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
     ++spi;
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
@@ -949,7 +950,8 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
   int64_t batch = std::max<int64_t>(1, budget / out_row_bytes);
   batch = std::min<int64_t>(batch, n);
   // several batches when there is enough work to overlap the copies
-  if (n >= 4096) batch = std::min<int64_t>(batch, (n + 5) / 6);
+  const int64_t nbatch_min = getenv("RK_E2E_BATCHES") ? std::max(1, atoi(getenv("RK_E2E_BATCHES"))) : 6;
+  if (n >= 4096) batch = std::min<int64_t>(batch, (n + nbatch_min - 1) / nbatch_min);
   if (!dx) {
     const size_t need = (size_t)(batch * in_row_bytes);
     if (need > w->in_cap) {
