@@ -273,11 +273,12 @@ def main():
         for _ in range(1):
             db.transform_into(x_host.data_ptr(), n, out_host.data_ptr(), bank.count * fpk, mode=args.mode)
         barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            db.transform_into(x_host.data_ptr(), n, out_host.data_ptr(), bank.count * fpk, mode=args.mode)
-            _ = float(out_host[n - 1, 1])  # the step's result read on the host
-        dt = time.perf_counter() - t0
+        with ClockSampler(local) as clk_e2e:
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                db.transform_into(x_host.data_ptr(), n, out_host.data_ptr(), bank.count * fpk, mode=args.mode)
+                _ = float(out_host[n - 1, 1])  # the step's result read on the host
+            dt = time.perf_counter() - t0
         t = torch.tensor([dt], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -286,7 +287,8 @@ def main():
                "h2d_bytes_per_step": int(x_host.numel() * 4),
                "d2h_bytes_per_step": int(out_host.numel() * 4),
                "ms_per_step": 1e3 * dt / args.steps,
-               "path": "DeviceBank.transform_into -> rk_transform_f32 (host pinned x/out, batched H2D/kernel/D2H)"}
+               "clocks": clk_e2e.summary(),
+               "path": "DeviceBank.transform_into -> rk_transform (host pinned x/out, pipelined H2D/kernel/D2H)"}
         del out_host
 
     # ---- CPU baseline on rank 0 at N=1 -------------------------------------

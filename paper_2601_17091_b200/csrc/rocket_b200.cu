@@ -339,7 +339,7 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   // chunk's weights and setup serve all of them
   const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 8;
   int spi = 1;
-  const int64_t min_items = getenv("RK_MIN_ITEMS") ? atoi(getenv("RK_MIN_ITEMS")) : 8;
+  const int64_t min_items = getenv("RK_MIN_ITEMS") ? atoi(getenv("RK_MIN_ITEMS")) : 2;
   while (spi < spi_max && n >= min_items * (spi + 1) * st->sms * ctas &&
          (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
     ++spi;
