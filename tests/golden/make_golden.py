@@ -90,6 +90,34 @@ def main():
             arrays[f"{name}/{variant}/executed"] = np.array([stats.total_dot_products], dtype=np.int64)
         print(name, values.shape, flush=True)
     np.savez_compressed(os.path.join(HERE, "transforms.npz"), **arrays)
+    make_ridge()
+
+
+def make_ridge():
+    """Reference ridge fits (ridge.py:100-242) on reference features of the
+    labelled fixture: a dual (features > rows) and a primal case, a
+    regression and an alpha selection."""
+    out = {}
+    ds = gr.synth_two_class(30, 64, seed=3)
+    labels = np.array(ds.labels)
+    for name, k in (("dual", 200), ("primal", 10)):
+        bank = gr.generate_bank(64, 1, k, gr.GenOptions(seed=0))
+        feats = gr.transform(ds, bank).values
+        m = gr.fit(feats, labels, alpha=1.0)
+        out[f"{name}/features"] = feats
+        out[f"{name}/weights"] = m.weights
+        out[f"{name}/intercepts"] = m.intercepts
+        out[f"{name}/means"] = m.feature_means
+        out[f"{name}/scales"] = m.feature_scales
+        out[f"{name}/predict"] = gr.predict(m, feats).astype(np.int64)
+        best, scores = gr.select_alpha(feats, labels, [0.01, 0.1, 1.0, 10.0], seed=4)
+        out[f"{name}/select_best"] = np.array([best])
+        out[f"{name}/select_scores"] = np.array([scores[a] for a in (0.01, 0.1, 1.0, 10.0)])
+        r = gr.fit_regression(feats, np.arange(feats.shape[0], dtype=np.float64), alpha=0.5)
+        out[f"{name}/reg_weights"] = r.weights
+        out[f"{name}/reg_intercepts"] = r.intercepts
+    out["labels"] = labels.astype(np.int64)
+    np.savez_compressed(os.path.join(HERE, "ridge.npz"), **out)
 
 
 if __name__ == "__main__":
