@@ -160,6 +160,28 @@ int64_t rk_run_batch_f64(const double* x, int64_t n_instances,
                          int32_t workers, int32_t fpk, double* out,
                          int64_t ld_out, int64_t row0);
 
+/* Streaming transform between files: the reference's
+ * `gridrocket transform` reads the whole dataset (load_dataset,
+ * data.py:293-302), transforms it in memory (cli.py:138-168) and saves the
+ * FeatureMatrix (features.py:59-67).  This entry point does the same work
+ * in bounded memory: n_series rows of n_channels*l_series values of type
+ * in_dtype are read from in_fd at byte in_offset (or, when in_fd < 0, from
+ * the host array x), converted to the compute dtype when they differ
+ * (float64 -> float32 rounds to nearest, like numpy's astype), transformed,
+ * and the (n_series, n_kernels*fpk) features of type dtype are written to
+ * out_fd at byte out_offset — the bytes FeatureMatrix.save writes after its
+ * header.  A reader thread (pread into pinned buffers), the GPU (H2D,
+ * transform, D2H on separate streams) and a writer thread (pwrite from
+ * pinned buffers) overlap batch by batch.  Non-finite inputs fail with
+ * RK_ERR_INVALID, as engine._check_shapes does (engine.py:252-268), after
+ * the rows before them were written.  batch_rows <= 0 picks a batch.
+ * *executed (may be NULL) = positions_per_series * n_series. */
+int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset,
+                        const void* x, int32_t in_dtype, int64_t n_series,
+                        int32_t out_fd, int64_t out_offset, int32_t dtype,
+                        int32_t fpk, int32_t mode, int64_t batch_rows,
+                        int64_t* executed);
+
 /* Release cached banks and per-device buffers (optional at exit). */
 int rk_release_caches(void);
 

@@ -9,6 +9,7 @@
 #include "../../include/rocket_b200.h"
 #include "transform_kernel.cuh"
 #include "kernel_tables.h"
+#include "rk_internal.h"
 
 #include <cuda_runtime.h>
 
@@ -547,6 +548,9 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
 extern "C" {
 
 int rk_abi_version(void) { return RK_ABI_VERSION; }
+
+// shared with the streaming runtime (rocket_stream.cu)
+int rk_set_error(int code, const char* message) { return fail(code, "%s", message); }
 
 const char* rk_last_error(void) { return g_last_error.c_str(); }
 
@@ -1166,6 +1170,7 @@ int64_t rk_run_batch_f64(const double* x, int64_t n_inst, int32_t C, int32_t L, 
 }
 
 int rk_release_caches(void) {
+  rk_stream_release();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (auto& kv : g_cache) rk_bank_destroy(kv.second);

@@ -91,6 +91,7 @@ def main():
         print(name, values.shape, flush=True)
     np.savez_compressed(os.path.join(HERE, "transforms.npz"), **arrays)
     make_ridge()
+    make_formats()
 
 
 def make_ridge():
@@ -118,6 +119,35 @@ def make_ridge():
         out[f"{name}/reg_intercepts"] = r.intercepts
     out["labels"] = labels.astype(np.int64)
     np.savez_compressed(os.path.join(HERE, "ridge.npz"), **out)
+
+
+def make_formats():
+    """Files written by the reference's own writers (_binio.py, kernels.py:
+    127-147, data.py:193-276, features.py:59-91) for the format parity
+    tests: a bank, dataset caches (f32 with labels, f64 without), .ts and
+    .csv exports, and feature files of reference transforms of the cached
+    dataset (single / single+MPV / double) plus one CSV export."""
+    from gridrocket.data import save_cache, write_csv, write_ts
+
+    out = os.path.join(HERE, "formats")
+    os.makedirs(out, exist_ok=True)
+    bank = gr.generate_bank(40, 1, 6, gr.GenOptions(seed=5))
+    bank.save(os.path.join(out, "bank_40x6.rkbk"))
+    gr.generate_bank(32, 3, 4, gr.GenOptions(seed=6, center_weights=False)).save(
+        os.path.join(out, "bank_3ch.rkbk"))
+    ds = gr.synth_two_class(3, 40, seed=8)
+    save_cache(ds, os.path.join(out, "two_class.rkds"))
+    write_ts(ds, os.path.join(out, "two_class.ts"))
+    write_csv(ds, os.path.join(out, "two_class.csv"))
+    ds64 = gr.Dataset(values=gr.synth_random(4, 1, 40, seed=9).values.astype(np.float64) * 1.5,
+                      name="random64")
+    save_cache(ds64, os.path.join(out, "random64.rkds"))
+    gr.transform(ds, bank).save(os.path.join(out, "two_class_single.rkfm"))
+    gr.transform(ds, bank, include_mpv=True).save(os.path.join(out, "two_class_mpv.rkfm"))
+    gr.transform(ds, bank, precision="double").save(os.path.join(out, "two_class_double.rkfm"))
+    gr.transform(ds64, bank).save(os.path.join(out, "random64_single.rkfm"))
+    gr.transform(ds, bank).to_csv(os.path.join(out, "two_class_single.csv"))
+    gr.transform(ds, bank, precision="double").to_csv(os.path.join(out, "two_class_double.csv"))
 
 
 if __name__ == "__main__":
