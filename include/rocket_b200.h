@@ -182,6 +182,26 @@ int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset,
                         int32_t fpk, int32_t mode, int64_t batch_rows,
                         int64_t* executed);
 
+/* Native bank generation: the reference's generate_bank
+ * (kernels.py:243-308) — numpy Generator(Philox(key=seed)) draws in the
+ * reference's per-kernel order (length, channel subset, weights, bias,
+ * dilation, padding) — replayed bit for bit in C++ on the host (no GPU).
+ * exponent_bounds[i] = float(np.log2((l_series-1)/(len_i-1))) for
+ * len = 7, 9, 11 and channel_bound = float(np.log2(n_channels)), computed by
+ * the caller with numpy as the reference does (kernels.py:204-214, 230-240).
+ * Per-kernel outputs have count entries; channel_indices and weights are
+ * filled up to index_capacity / weight_capacity (count*n_channels and
+ * count*11*n_channels always suffice) and *n_indices / *n_weights receive
+ * the lengths used.  Returns RK_ERR_CAPACITY if a buffer is too small. */
+int rk_generate_bank(int64_t count, int32_t l_series, int32_t n_channels,
+                     uint64_t seed, int32_t center_weights,
+                     const double* exponent_bounds, double channel_bound,
+                     int32_t* lengths, double* biases, int32_t* dilations,
+                     int32_t* paddings, int32_t* channel_counts,
+                     int32_t* channel_indices, int64_t index_capacity,
+                     double* weights, int64_t weight_capacity,
+                     int64_t* n_weights, int64_t* n_indices);
+
 /* Release cached banks and per-device buffers (optional at exit). */
 int rk_release_caches(void);
 

@@ -42,6 +42,7 @@ EXPORTS = (
     "rk_run_batch_f64",
     "rk_release_caches",
     "rk_transform_stream",
+    "rk_generate_bank",
 )
 
 NVCC_FLAGS = [
@@ -82,7 +83,9 @@ def build(verbose=False, out=None, defines=()):
     os.makedirs(objdir, exist_ok=True)
     flags = [*NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE]
     units = [("rocket_b200.o", os.path.join(CSRC, "rocket_b200.cu"), []),
-             ("rocket_stream.o", os.path.join(CSRC, "rocket_stream.cu"), [])]
+             ("rocket_stream.o", os.path.join(CSRC, "rocket_stream.cu"), []),
+             # host-only; no FMA contraction so the doubles round like numpy's
+             ("bank_gen.o", os.path.join(CSRC, "bank_gen.cpp"), ["-Xcompiler", "-ffp-contract=off"])]
     units += [(f"kernels_len{n}.o", os.path.join(CSRC, "kernels_len.cu"), [f"-DRK_LEN={n}"]) for n in (7, 9, 11)]
     procs = []
     for obj, src, extra in units:
@@ -140,6 +143,9 @@ def load():
     lib.rk_transform_f32.argtypes = [p, p, i64, p, i64, i64, i32, i32, p, ctypes.POINTER(i64)]
     lib.rk_transform_stream.restype = ctypes.c_int
     lib.rk_transform_stream.argtypes = [p, i32, i64, p, i32, i64, i32, i64, i32, i32, i32, i64, ctypes.POINTER(i64)]
+    lib.rk_generate_bank.restype = ctypes.c_int
+    lib.rk_generate_bank.argtypes = [i64, i32, i32, ctypes.c_uint64, i32, p, ctypes.c_double, p, p, p, p, p, p, i64,
+                                     p, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.rk_run_batch_f32.restype = i64
     lib.rk_run_batch_f32.argtypes = [p, i64, i32, i32, p, p, p, p, p, p, p, p, p, i64, i32, i32, p, i64, i64]
     lib.rk_release_caches.restype = ctypes.c_int
