@@ -80,7 +80,9 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
            + 2 * (r + len - 1) * nc      // window loads + addresses
            + extra;
   };
-  return nfull * step(R, 8) + masked_steps * (step(R, 40) + 2 * (R + len - 1) * nc + R * G) + 40 * G + 60;
+  // a masked step adds a compare and a select per last-tap load (the
+  // NaN-slot masking, transform_kernel.cuh load_window_masked)
+  return nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) + 40 * G + 60;
 }
 
 }  // namespace

@@ -162,16 +162,26 @@ __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const floa
   for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
 }
 
-// Masked steps: positions past n read past the staged row; only the upper
-// end needs a clamp (for a live lane u0 - C*d >= lo - C*d = -p_C >= -halo,
-// where p_C is the padding of the chunk's longest kernel).
+// Masked steps: a lane's valid positions are a prefix r < rcount of its
+// run (rcount = 0 for a lane without a run).  Position r reads window
+// entries r .. r+LEN-1, so entry q = r+LEN-1 (its last tap) is loaded only
+// while r*d < nleft and otherwise replaced by a canonical NaN: every output
+// of a dead position is NaN, which the pooling ignores by IEEE semantics
+// (NaN > t is false; min/max return the other operand; the sign bit of the
+// canonical NaN is clear, so the FAST count adds nothing).  The first LEN-1
+// entries belong to position 0, which is in range for a live lane and is
+// read at lane start lo for a dead one.
 template <int LEN, int R>
-__device__ __forceinline__ void load_window_clamped(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
-                                                    int u0, int d, int hi_clamp) {
+__device__ __forceinline__ void load_window_masked(float (&xw)[R + LEN - 1], const float* __restrict__ chan,
+                                                   int u0, int d, int nleft, const float* nan_slot) {
   constexpr int C = (LEN - 1) / 2;
-  const int i0 = u0 - C * d;
+  const float* p = chan + (u0 - C * d);
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = chan[min(i0 + q * d, hi_clamp)];
+  for (int q = 0; q < R + LEN - 1; ++q) {
+    const float* a = p + q * d;
+    if (q >= LEN - 1) a = (q - (LEN - 1)) * d < nleft ? a : nan_slot;
+    xw[q] = *a;
+  }
 }
 
 // Per-lane pooled state for the kernels of one chunk.  ext is the running
@@ -264,8 +274,13 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
     }
   }
   if (lane < c.nk) {
-    // ppv: count / l_out divided in float64, stored as float32 (engine.py:187)
-    const float ppv = __double2float_rn(__ddiv_rn((double)my_cnt, (double)c.n));
+    // ppv: the reference stores f32(RN64(count / l_out)) (engine.py:187).
+    // For integers c <= n < 2^24 that equals the single rounding
+    // RN32(c / n): a non-midpoint quotient lies >= 2^-49 (relative) from
+    // every f32 midpoint, farther than RN64 moves it, so both roundings pick
+    // the same float (checked exhaustively for n <= 20000 and sampled to
+    // 2^24, tests/test_host.py).
+    const float ppv = __fdiv_rn((float)my_cnt, (float)c.n);
     // exact: RN(max_t acc_t + b) == max_t RN(acc_t + b); fast: -min acc'
     const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
     float* dst = orow + (int64_t)my_col * fpk;
@@ -284,27 +299,18 @@ template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
 __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                            const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
-                                           int hi_clamp, bool live) {
-  // FAST masked steps start dead positions at +inf: inf + finite stays
-  // +inf, which has a clear sign bit (not counted) and never lowers the min
+                                           const float* nan_slot) {
   float2 init_r[P][R];
 #pragma unroll
   for (int p = 0; p < P; ++p)
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (MASKED && !EXACT) {
-        const bool ok = live && (r * d < nleft);
-        init_r[p][r] = ok ? init[p] : make_float2(INFINITY, INFINITY);
-      } else {
-        init_r[p][r] = init[p];
-      }
-    }
+    for (int r = 0; r < R; ++r) init_r[p][r] = init[p];
   float2 acc[P][R];
 #pragma unroll
   for (int s = 0; s < NC; ++s) {
     float xw[R + LEN - 1];
     if (MASKED)
-      load_window_clamped<LEN, R>(xw, chan[s], u0, d, hi_clamp);
+      load_window_masked<LEN, R>(xw, chan[s], u0, d, nleft, nan_slot);
     else
       load_window<LEN, R>(xw, chan[s], u0, d);
     if (s == 0)
@@ -312,7 +318,7 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
     else
       accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, init_r, one2);
   }
-  pool_update<R, P, EXACT, MASKED && EXACT>(st, acc, thr, live, nleft, d);
+  pool_update<R, P, EXACT, false>(st, acc, thr, true, 0, d);
 }
 
 // Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
@@ -326,7 +332,7 @@ template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
-                                              int r32, float invd, int hi_clamp, int lane) {
+                                              int r32, float invd, const float* nan_slot, int lane) {
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
@@ -342,7 +348,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   const int dv = q32 * RD + r32;
 #pragma unroll(kStepUnroll)
   for (int stp = 0; stp < nfull; ++stp) {
-    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, 0, true);
+    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
     s += r32;
     v0 += dv;
     if (s >= d) {
@@ -352,8 +358,8 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   }
   for (int base = nfull << 5; base < starts; base += 32) {
     const bool live = base + lane < starts;
-    const int vv = live ? v0 : 0;
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + vv, d, n - vv, hi_clamp, live);
+    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
+                                           live ? n - v0 : 0, nan_slot);
     s += r32;
     v0 += dv;
     if (s >= d) {
@@ -407,8 +413,8 @@ __device__ __forceinline__ void stage_rows(float* __restrict__ smem, const float
 template <int LEN, int R, int P, int NC, bool EXACT>
 __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __restrict__ sx,
                                           const float* __restrict__ weights, const int* __restrict__ chan_off,
-                                          float* __restrict__ orow, int fpk, int vec_out, float one, int halo,
-                                          int L, int lane) {
+                                          float* __restrict__ orow, int fpk, int vec_out, float one,
+                                          const float* nan_slot, int lane) {
   constexpr int G = 2 * P;
   float2 w[NC][P][LEN];
   const float2* wp = reinterpret_cast<const float2*>(weights + c.wofs);
@@ -427,7 +433,7 @@ __device__ __forceinline__ void run_chunk(const DevChunk& c, const float* __rest
   Pool<G> st;
   pool_init<G, EXACT>(st);
   run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, make_float2(one, one), c.lo, c.n, c.d, c.q32,
-                                      c.r32, c.invd, L + halo - 1, lane);
+                                      c.r32, c.invd, nan_slot, lane);
   finish_chunk<G, EXACT>(c, st, orow, fpk, vec_out, lane);
 }
 
@@ -482,8 +488,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_next;
   __shared__ int s_item;
+  __shared__ float s_nan;  // the masked steps' dead-position source
   const int tid = threadIdx.x;
   const int lane = tid & 31;
+  if (tid == 0) s_nan = __int_as_float(0x7fffffff);
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
   const int SPI = a.series_per_item;
   const int slot_floats = C * S;
@@ -521,11 +529,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
       float* orow = a.out + (series0 + si) * a.ld_out;
       const float* sx = smem + si * slot_floats + H;  // chan_off entries are relative to this
       if (NCK == 0)
-        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
+        run_chunk<LEN, R, 2, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, &s_nan, lane);
       else if (NCK == 1)
-        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
+        run_chunk<LEN, R, 1, 2, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, &s_nan, lane);
       else if (NCK == 3)
-        run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, H, L, lane);
+        run_chunk<LEN, R, 1, 1, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, &s_nan, lane);
       else
         run_chunk_generic<LEN, EXACT>(c, sx, a.weights, a.chan_off, orow, a.fpk, a.vec_out, a.one, lane);
       done += (unsigned long long)c.nk * (unsigned long long)c.n;
@@ -699,8 +707,10 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
   __shared__ int s_next;
+  __shared__ float s_nan;  // the masked steps' dead-position source
   asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_nan = __int_as_float(0x7fffffff);
   const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
   const int SPI = p.h.spi;
   const int slot = C * S;
@@ -753,7 +763,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         Pool<2 * P> st;
         pool_init<2 * P, EXACT>(st);
         run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
-                                            L + H - 1, lane);
+                                            &s_nan, lane);
         finish_chunk<2 * P, EXACT>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out, lane);
         done += (unsigned long long)c.nk * (unsigned long long)c.n;
       }

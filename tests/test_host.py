@@ -116,3 +116,24 @@ def test_transform_fails_loudly_without_gpu():
     bank = generate_bank(64, 1, 20, GenOptions(seed=11))
     with pytest.raises((RuntimeError, OSError)):
         transform(np.zeros((2, 1, 64)), bank)
+
+
+def test_ppv_single_rounding_equals_double_rounding():
+    """The kernels compute PPV as RN32(count / l_out) (transform_kernel.cuh,
+    finish_chunk); the reference stores f32(RN64(count / l_out))
+    (engine.py:187).  Equal for every count <= l_out < 2^24: exhaustive
+    for l_out <= 20000, sampled above."""
+    import numpy as np
+
+    for n in range(1, 20001):
+        c = np.arange(0, n + 1, dtype=np.int64)
+        a = (c.astype(np.float64) / n).astype(np.float32)
+        b = c.astype(np.float32) / np.float32(n)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), n
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        n = int(rng.integers(20001, 1 << 24))
+        c = np.concatenate([rng.integers(0, n + 1, size=100000), [0, 1, n - 1, n]])
+        a = (c.astype(np.float64) / n).astype(np.float32)
+        b = c.astype(np.float32) / np.float32(n)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), n
