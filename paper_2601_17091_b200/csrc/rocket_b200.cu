@@ -123,6 +123,7 @@ struct rk_bank_s {
   double* d_cw64 = nullptr;
   double* d_cb64 = nullptr;
   std::vector<int64_t> cell_order;  // sorted position -> bank index
+  int64_t cell_len_begin[3] = {}, cell_len_end[3] = {};  // sorted range per length 7/9/11
   int64_t n_weights = 0;
   int64_t device_bytes = 0;
   std::map<std::pair<int, int>, int*> d_block_start;  // (class, n_blocks) -> device boundaries
@@ -416,10 +417,49 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
 }
 
 // Cell path: precision "double" (esz 8) or MPV (fpk 3).
-int launch_cells(rk_bank_t b, const void* d_x, int esz, int64_t n, void* d_out, int64_t ld_out, int fpk,
-                 cudaStream_t stream, unsigned long long* d_exec) {
+// float64 (precision "double") and MPV (fpk = 3): the reference loop order
+// on the CUDA cores.  The staged cell kernel (one series in shared memory,
+// one launch per kernel length) when a series fits; otherwise the unstaged
+// cell kernel reading the series from global memory.
+#ifndef RK_CELL_B
+#define RK_CELL_B 4  // positions per block (independent accumulation chains)
+#endif
+template <typename T, bool MPV, int LEN>
+int launch_cellrow(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStream_t stream) {
+  auto fn = rk::rocket_cellrow_kernel<T, MPV, LEN, RK_CELL_B>;
+  int rc = set_kernel_smem(st, (const void*)fn, (int)smem);
+  if (rc) return rc;
+  int per_sm = 1;
+  RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+  const int64_t grid = std::min<int64_t>(a.n_series, (int64_t)st->sms * std::max(1, per_sm));
+  fn<<<(unsigned)grid, 256, smem, stream>>>(a);
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
+template <typename T, bool MPV>
+int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t stream, int* d_counters) {
+  const size_t smem = (size_t)b->C * b->sstride * sizeof(T);
+  RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * 3, stream));
+  a.halo = b->halo;
+  a.sstride = b->sstride;
+  for (int li = 0; li < 3; ++li) {
+    if (b->cell_len_end[li] <= b->cell_len_begin[li]) continue;
+    a.k_begin = (int)b->cell_len_begin[li];
+    a.k_end = (int)b->cell_len_end[li];
+    a.item_counter = d_counters + li;
+    const int rc = li == 0 ? launch_cellrow<T, MPV, 7>(st, a, smem, stream)
+                 : li == 1 ? launch_cellrow<T, MPV, 9>(st, a, smem, stream)
+                           : launch_cellrow<T, MPV, 11>(st, a, smem, stream);
+    if (rc) return rc;
+  }
+  return RK_OK;
+}
+
+int launch_cells(rk_bank_t b, DeviceState* st, const void* d_x, int esz, int64_t n, void* d_out, int64_t ld_out,
+                 int fpk, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
   if (esz == 8 && !b->d_cw64) return fail(RK_ERR_INVALID, "double precision needs rk_bank_attach_f64 first");
-  rk::CellArgs a;
+  rk::CellArgs a = {};
   a.x = d_x;
   a.out = d_out;
   a.ld_out = ld_out;
@@ -433,6 +473,13 @@ int launch_cells(rk_bank_t b, const void* d_x, int esz, int64_t n, void* d_out, 
   a.l_series = b->L;
   a.n_channels = b->C;
   a.fpk = fpk;
+  const size_t staged = (size_t)b->C * b->sstride * esz;
+  if (staged + 1024 <= st->smem_optin && !getenv("RK_NO_CELLROW")) {
+    if (esz == 8)
+      return fpk == 3 ? launch_cellrows<double, true>(b, st, a, stream, d_counters)
+                      : launch_cellrows<double, false>(b, st, a, stream, d_counters);
+    return launch_cellrows<float, true>(b, st, a, stream, d_counters);
+  }
   dim3 grid((unsigned)((b->K + 127) / 128), (unsigned)std::min<int64_t>(n, 65535));
   if (esz == 8) {
     if (fpk == 3)
@@ -449,7 +496,7 @@ int launch_cells(rk_bank_t b, const void* d_x, int esz, int64_t n, void* d_out, 
 int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_outv, int64_t ld_out, int fpk,
            int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters, int esz) {
   if (n <= 0) return RK_OK;
-  if (esz == 8 || fpk == 3) return launch_cells(b, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec);
+  if (esz == 8 || fpk == 3) return launch_cells(b, st, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec, d_counters);
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
@@ -844,11 +891,21 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     b->cell_order.resize(K);
     for (int64_t k = 0; k < K; ++k) b->cell_order[k] = k;
     auto l_out_of = [&](int64_t k) { return (int64_t)L + 2 * paddings[k] - (int64_t)(lengths[k] - 1) * dilations[k]; };
+    // (length, channels, dilation, padding): a warp of the staged cell
+    // kernel gets one length and mostly one (d, p), so its lanes read the
+    // same shared-memory words and run equal trip counts
     std::stable_sort(b->cell_order.begin(), b->cell_order.end(), [&](int64_t x, int64_t y) {
-      const int64_t tx = (int64_t)lengths[x] * chcnt[x], ty = (int64_t)lengths[y] * chcnt[y];
-      if (tx != ty) return tx > ty;
-      return l_out_of(x) > l_out_of(y);
+      return std::make_tuple(lengths[x], chcnt[x], dilations[x], paddings[x]) <
+             std::make_tuple(lengths[y], chcnt[y], dilations[y], paddings[y]);
     });
+    for (int li = 0; li < 3; ++li) {
+      b->cell_len_begin[li] = b->cell_len_end[li] = 0;
+    }
+    for (int64_t i = 0; i < K; ++i) {
+      const int li = kLenIdx[lengths[b->cell_order[i]]];
+      if (i == 0 || kLenIdx[lengths[b->cell_order[i - 1]]] != li) b->cell_len_begin[li] = i;
+      b->cell_len_end[li] = i + 1;
+    }
     std::vector<rk::CellKernel> ck(K);
     std::vector<float> cb(K);
     for (int64_t i = 0; i < K; ++i) {

@@ -623,6 +623,11 @@ struct CellArgs {
   int l_series;
   int n_channels;
   int fpk;
+  // staged variant (rocket_cellrow_kernel)
+  int* item_counter;     // dynamic series scheduler (zeroed before the launch)
+  int k_begin, k_end;    // sorted-kernel range of this launch (one length)
+  int halo;              // zero halo per side of a staged row (elements)
+  int sstride;           // elements per staged channel row
 };
 
 template <typename T>
@@ -686,6 +691,130 @@ __global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(kFull, done, o);
   if ((threadIdx.x & 31) == 0 && done) atomicAdd(a.executed, done);
+}
+
+// Staged cell kernel: a CTA stages one series (all channels, zero halos)
+// in shared memory; each warp takes 32 consecutive sorted kernels of one
+// length LEN, one kernel per lane, and walks the positions in ascending
+// order, B at a time (B independent accumulation chains).  Per position
+// the arithmetic is the reference's: acc = +0, then RN(acc + RN(w*x)) over
+// channels and taps in order, RN(acc + b), the positive sum in position
+// order.  Out-of-range taps read the zero halo instead of being skipped:
+// RN(w*0) is a signed zero and acc is never -0 (it starts at +0 and an RN
+// sum is -0 only for -0 + -0), so acc + (+-0) == acc bit for bit.  Kernels
+// are sorted by (length, channels, dilation, padding) so the lanes of a
+// warp mostly read the same smem word (a broadcast) and run equal trip
+// counts.
+template <typename T, bool MPV, int LEN, int B>
+__global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
+  extern __shared__ __align__(16) unsigned char cell_smem[];
+  T* xs = reinterpret_cast<T*>(cell_smem);
+  __shared__ int s_item, s_next;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
+  for (int k = tid; k < C * S; k += blockDim.x) {
+    const int t = k % S;
+    if (t < H || t >= H + L) xs[k] = T(0);
+  }
+  const int ngroups = (a.k_end - a.k_begin + 31) / 32;
+  const T* wts = reinterpret_cast<const T*>(a.weights);
+  const T* bis = reinterpret_cast<const T*>(a.biases);
+  unsigned long long done = 0;
+  while (true) {
+    __syncthreads();  // every warp has left the previous series
+    if (tid == 0) {
+      s_item = atomicAdd(a.item_counter, 1);
+      s_next = 0;
+    }
+    __syncthreads();
+    const int64_t i = s_item;
+    if (i >= a.n_series) break;
+    const T* xi = reinterpret_cast<const T*>(a.x) + i * (int64_t)C * L;
+    for (int k = tid; k < C * L; k += blockDim.x) {
+      const int c = k / L, t = k - c * L;
+      xs[c * S + H + t] = xi[k];
+    }
+    __syncthreads();
+    while (true) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(&s_next, 1);
+      g = __shfl_sync(kFull, g, 0);
+      if (g >= ngroups) break;
+      const int ks = a.k_begin + g * 32 + lane;
+      const bool live = ks < a.k_end;
+      const CellKernel kd = a.kernels[live ? ks : a.k_begin + g * 32];
+      const int lout = live ? kd.l_out : 0;
+      const int span = __reduce_max_sync(kFull, lout);
+      const T bias = bis[live ? ks : a.k_begin + g * 32];
+      const T* wk = wts + kd.woff;
+      T w0[LEN];  // slot-0 weights, kept for the whole walk
+#pragma unroll
+      for (int j = 0; j < LEN; ++j) w0[j] = wk[j];
+      const T* x0 = xs + __ldg(a.chidx + kd.choff) * S + H - kd.p;
+      int count = 0;
+      T mx = T(-INFINITY), psum = T(0);
+      for (int t0 = 0; t0 < span; t0 += B) {
+        T acc[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = T(0);
+        // dead positions (t >= l_out) re-read the last live window
+        const int tb = min(t0, max(lout - B, 0));
+#pragma unroll
+        for (int j = 0; j < LEN; ++j) {
+          const T* xp = x0 + tb + j * kd.d;
+#pragma unroll
+          for (int b = 0; b < B; ++b) acc[b] = add_rn<T>(acc[b], mul_rn<T>(w0[j], xp[b]));
+        }
+        for (int c = 1; c < kd.nc; ++c) {
+          const T* xc = xs + __ldg(a.chidx + kd.choff + c) * S + H - kd.p + tb;
+          const T* wc = wk + c * LEN;
+#pragma unroll
+          for (int j = 0; j < LEN; ++j) {
+            const T wj = wc[j];
+#pragma unroll
+            for (int b = 0; b < B; ++b) acc[b] = add_rn<T>(acc[b], mul_rn<T>(wj, xc[j * kd.d + b]));
+          }
+        }
+        // position t0 + b is live iff t0 + b < lout; its accumulator is
+        // acc[t0 + b - tb] (tb < t0 only in a lane's final, shifted block)
+        const int shift = t0 - tb;
+        auto pool = [&](T v) {
+          v = add_rn<T>(v, bias);
+          if (v > T(0)) {
+            ++count;
+            if (MPV) psum = add_rn<T>(psum, v);
+          }
+          if (v > mx) mx = v;
+        };
+        if (shift == 0) {
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            if (t0 + b < lout) pool(acc[b]);
+        } else {
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const int q = b + shift;
+            if (t0 + b < lout) {
+              T v = acc[0];
+#pragma unroll
+              for (int r = 1; r < B; ++r) v = q == r ? acc[r] : v;
+              pool(v);
+            }
+          }
+        }
+      }
+      if (live) {
+        T* o = reinterpret_cast<T*>(a.out) + i * a.ld_out + (int64_t)kd.col * a.fpk;
+        o[0] = from_double<T>((double)count / (double)kd.l_out);
+        o[1] = mx;
+        if (MPV) o[2] = count > 0 ? from_double<T>((double)psum / (double)count) : T(0);
+        done += (unsigned long long)kd.l_out;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(kFull, done, o);
+  if (lane == 0 && done) atomicAdd(a.executed, done);
 }
 
 }  // namespace rk

@@ -207,6 +207,32 @@ def test_mpv_and_double_config2_rows_vs_oracle(cuda_ready):
     assert dbl.tobytes() == oracle_transform(values, bank, precision="double").tobytes()
 
 
+def test_staged_and_unstaged_cell_kernels_agree(cuda_ready, monkeypatch):
+    """The staged cell kernel (series in shared memory) and the unstaged one
+    (its fallback when a series does not fit) are both the reference's loop:
+    identical bytes, multichannel MPV and double."""
+    bank = generate_bank(96, 5, 300, GenOptions(seed=21))
+    values = synth_random(40, 5, 96, seed=22).values
+    staged = [transform(values, bank, include_mpv=True).values,
+              transform(values, bank, precision="double", include_mpv=True).values]
+    monkeypatch.setenv("RK_NO_CELLROW", "1")
+    unstaged = [transform(values, bank, include_mpv=True).values,
+                transform(values, bank, precision="double", include_mpv=True).values]
+    for a, b in zip(staged, unstaged):
+        assert a.tobytes() == b.tobytes()
+
+
+def test_double_long_series_vs_oracle(cuda_ready):
+    """L = 16384 in float64 needs more shared memory than an SM has for one
+    staged series: the unstaged cell kernel runs, still byte-identical."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(16384, 1, 120, GenOptions(seed=0))
+    values = synth_random(2, 1, 16384, seed=1).values
+    out = transform(values, bank, precision="double", include_mpv=True).values
+    assert out.tobytes() == oracle_transform(values, bank, precision="double", include_mpv=True).tobytes()
+
+
 def test_run_batch_f64_dropin(golden_transforms, cuda_ready):
     lib = cuda_ready
     values, bank = _case("rc5")

@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches <launches.csv> <out.json>
     python tools/ncu_summary.py report <prof.ncu-rep> <out.txt>
+    python tools/ncu_summary.py bench <launches.csv> <out.json>   (a whole bench.py run, per kernel name)
 """
 import csv
 import json
@@ -102,5 +103,31 @@ def report(src, dst):
     print("\n".join(lines))
 
 
+def bench(src, dst):
+    """Launch list of a whole `bench.py` run under ncu: per-kernel-name launch
+    counts, total and mean durations, and each name's share of the
+    library's GPU time (the serialised, cold-cache ncu times)."""
+    launches(src, dst + ".tmp", skip_first_half=False)
+    data = json.load(open(dst + ".tmp"))
+    import os
+
+    os.remove(dst + ".tmp")
+    agg = {}
+    for k in data["kernels"]:
+        name = k["kernel"].split("(")[0]
+        a = agg.setdefault(name, {"kernel": name, "launches": 0, "ns": 0.0})
+        a["launches"] += 1
+        a["ns"] += k["ns"]
+    tot = sum(a["ns"] for a in agg.values()) or 1
+    rows = sorted(agg.values(), key=lambda a: -a["ns"])
+    for a in rows:
+        a["share"] = a["ns"] / tot
+        a["mean_ns"] = a["ns"] / a["launches"]
+    json.dump({"launches": data["launches"], "total_ns": tot, "by_kernel": rows, "per_launch": data["kernels"]},
+              open(dst, "w"), indent=1)
+    for a in rows:
+        print(f"{a['kernel'][:70]:70s} {a['launches']:5d} {a['ns']/1e6:9.2f} ms {a['share']:.1%}")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "report": report, "bench": bench}[sys.argv[1]](sys.argv[2], sys.argv[3])
