@@ -209,9 +209,16 @@ def main():
     from paper_2601_17091_b200 import GenOptions, device_bank, generate_bank, synth_random
 
     rank, world, local = dist_env()
+    # one process per GPU; the modulo only matters for a logic check of the
+    # multi-rank path on a box with fewer GPUs than ranks
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("RK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     bank = generate_bank(cfg["l"], cfg["c"], cfg["k"], GenOptions(seed=0))
     db = device_bank(bank, local)
@@ -341,6 +348,9 @@ def main():
             "roofline": {"bound": "fp32", "achieved": achieved_tflops, "peak": FP32_PEAK_MEASURED,
                          "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_MEASURED, "traffic": traffic,
                          "flops_per_series": flops_series,
+                         "algorithmic_bytes": (4 * cfg["c"] * cfg["l"] + 4 * fpk * bank.count) * n,
+                         "traffic_source": "profiles/ncu_summary_%s.json (ncu dram bytes of one transform, "
+                                           "scaled to this step's series)" % args.config if traffic else None,
                          "peak_source": "measured FFMA2 microbenchmark (profiles/r01_fp32_peak_microbench.jsonl); "
                                         "MEASURED_PEAKS.json has no FP32 entry",
                          "kernel": ("rocket_wide_kernel" if info["path"] == 1 else "rocket_class_kernel")
