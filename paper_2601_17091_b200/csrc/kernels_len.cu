@@ -9,29 +9,33 @@
 namespace {
 constexpr int kLenIdx = (RK_LEN - 7) / 2;
 
-template <int R, int NCK>
+// Exact mode never runs R above r_of(kExactRIdxCap) (exec_cls caps it), so
+// those exact variants are not instantiated.
+template <int RI, int NCK>
 void fill_class(rk::KernelFn* t, int cls) {
+  constexpr int R = rk::r_of(RI);
   t[2 * cls + 0] = rk::rocket_class_kernel<RK_LEN, R, NCK, false>;
-  t[2 * cls + 1] = rk::rocket_class_kernel<RK_LEN, R, NCK, true>;
+  if constexpr (RI <= rk::kExactRIdxCap) t[2 * cls + 1] = rk::rocket_class_kernel<RK_LEN, R, NCK, true>;
 }
 
-template <int R, int P, int NC>
+template <int RI, int P, int NC>
 void fill_wide(rk::WarpFn* wide, int cls) {
+  constexpr int R = rk::r_of(RI);
   wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false>;
-  wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
+  if constexpr (RI <= rk::kExactRIdxCap) wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
 }
 
 template <int RI>
 void fill_r(rk::KernelFn* ct, rk::WarpFn* dt) {
   constexpr int R = rk::r_of(RI);
   const int base = (kLenIdx * rk::kNumR + RI) * rk::kNumNck;
-  fill_class<R, 0>(ct, base + 0);
-  fill_class<R, 1>(ct, base + 1);
-  fill_class<R, 3>(ct, base + 3);
-  if constexpr (R == 1) fill_class<R, 2>(ct, base + 2);  // generic channels: 1 position per lane
-  fill_wide<R, 2, 1>(dt, base + 0);
-  fill_wide<R, 1, 2>(dt, base + 1);
-  fill_wide<R, 1, 1>(dt, base + 3);
+  fill_class<RI, 0>(ct, base + 0);
+  fill_class<RI, 1>(ct, base + 1);
+  fill_class<RI, 3>(ct, base + 3);
+  if constexpr (R == 1) fill_class<RI, 2>(ct, base + 2);  // generic channels: 1 position per lane
+  fill_wide<RI, 2, 1>(dt, base + 0);
+  fill_wide<RI, 1, 2>(dt, base + 1);
+  fill_wide<RI, 1, 1>(dt, base + 3);
 }
 }  // namespace
 

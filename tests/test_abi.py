@@ -53,3 +53,36 @@ def test_run_batch_rejects_bad_workers():
     rc = lib.rk_run_batch_f32(None, 0, 1, 64, None, None, None, None, None, None, None, None, None, 1, 0, 2, None,
                               2, 0)
     assert rc == -_lib.RK_ERR_INVALID
+
+
+def test_wide_kernels_do_not_spill():
+    """The wide kernel relies on warp-uniform chunk indices (weights in
+    uniform registers) and ~80 vector registers; a change that breaks either
+    shows up as a stack frame / local-memory spills in the compiled
+    objects (a 35 % slowdown when it happened)."""
+    import glob
+    import shutil
+    import subprocess
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    objs = glob.glob(os.path.join(os.path.dirname(_lib.LIB_PATH), "obj_librocket_b200", "kernels_len*.o"))
+    if not objs:
+        pytest.fail("kernel objects not built (run __graft_entry__.build())")
+    bad = []
+    for obj in objs:
+        out = subprocess.run(["cuobjdump", "-res-usage", obj], capture_output=True, text=True).stdout
+        name = None
+        for line in out.splitlines():
+            if "Function" in line:
+                name = line.split("Function")[-1].strip(" :")
+            elif "REG:" in line and name and "wide_kernel" in name:
+                fields = dict(f.split(":") for f in line.split() if ":" in f)
+                # fast-mode variants (template flag EXACT = false, "Lb0E")
+                # must not spill at all; a few exact-mode variants keep a
+                # spill of <= 24 bytes outside the step loop.  The regression
+                # this guards against was 120+ bytes.
+                limit = 0 if "Lb0EEEv" in name else 32
+                if int(fields.get("STACK", 0)) > limit or int(fields.get("LOCAL", 0)):
+                    bad.append((name, line.strip()))
+    assert not bad, bad[:3]
