@@ -106,7 +106,8 @@ struct rk_bank_s {
     int cls;
     int n_chunks;
     int64_t dense_flops;  // 2 * taps * positions of one series (diagnostics)
-    std::vector<rk::float4_t> blob;
+    std::vector<rk::float4_t> blob;       // exact mode
+    std::vector<rk::float4_t> blob_fast;  // fast mode: weights negated (the series is staged as is)
   };
   bool wide_path = false;  // parameter-block launches, W warps share a series
   int wide_ctas_per_sm = 0;  // default CTAs per SM (many series)
@@ -376,7 +377,7 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     h.one = 1.0f;
     h.wbytes = NC * P * len * 8;
     h.spi = spi;
-    std::memcpy(params.blob, wl.blob.data(), sizeof(params.blob));
+    std::memcpy(params.blob, exact ? wl.blob.data() : wl.blob_fast.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(32 * warps);
@@ -859,6 +860,13 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
             std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
             wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
           }
+          // fast mode computes acc' = -b + sum (-w) x; (-w) * x == w * (-x)
+          // bit for bit, so negating the weights replaces negating the
+          // staged series and lets the rows be bulk-copied unchanged
+          wl.blob_fast = wl.blob;
+          float* wf = reinterpret_cast<float*>(reinterpret_cast<char*>(wl.blob_fast.data()) +
+                                               (size_t)nch * sizeof(rk::WChunk));
+          for (size_t q = 0; q < (size_t)nch * wbytes / sizeof(float); ++q) wf[q] = -wf[q];
           b->wide_launches.push_back(std::move(wl));
         }
       }

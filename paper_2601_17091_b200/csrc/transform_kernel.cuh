@@ -831,15 +831,48 @@ namespace rk {
 
 constexpr int kWideMaxWarps = 24;
 
+// 1-D TMA (cp.async.bulk) staging of whole series rows, completed on an
+// mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 template <int LEN, int R, int P, int NC, bool EXACT>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
   __shared__ int s_next;
   __shared__ float s_nan;  // the masked steps' dead-position source
+  __shared__ __align__(8) unsigned long long s_bar;  // TMA staging barrier
   asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) s_nan = __int_as_float(0x7fffffff);
+  const unsigned bar = smem_u32(&s_bar);
+  unsigned phase = 0;
+  if (tid == 0) {
+    s_nan = __int_as_float(0x7fffffff);
+    if (p.h.vec_in) mbar_init(bar, 1);
+  }
   const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
   const int SPI = p.h.spi;
   const int slot = C * S;
@@ -862,8 +895,23 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
     if (series0 >= p.h.n_series) break;
     const int64_t left = p.h.n_series - series0;
     const int ns = left < SPI ? (int)left : SPI;
-    stage_rows<EXACT>(smem, p.h.x + series0 * C * L, ns * C, L, S, H, p.h.vec_in, tid, blockDim.x);
-    __syncthreads();
+    // Stage the item's rows unchanged (FAST negates the weights instead of
+    // the series): one bulk copy per row when rows are 16-byte aligned,
+    // else a cooperative copy.
+    if (p.h.vec_in) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
+        const unsigned row_bytes = (unsigned)L * 4u;
+        mbar_expect_tx(bar, row_bytes * (unsigned)(ns * C));
+        const float* src = p.h.x + series0 * C * L;
+        for (int r = 0; r < ns * C; ++r) tma_row(smem_u32(smem + r * S + H), src + (int64_t)r * L, row_bytes, bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+    } else {
+      stage_rows<true>(smem, p.h.x + series0 * C * L, ns * C, L, S, H, 0, tid, blockDim.x);
+      __syncthreads();
+    }
     while (true) {
       int ci = 0;
       if (lane == 0) ci = atomicAdd(&s_next, 1);
