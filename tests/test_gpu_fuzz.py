@@ -1,0 +1,89 @@
+"""Randomised parity sweep on the GPU against the C oracle (the restatement
+of engine._run_batch pinned to the reference's golden vectors): random
+series lengths (odd, even, not multiples of 4), channel counts, kernel
+counts, seeds, centring and series counts, in every path — exact (bytes),
+fast (tolerance), MPV and float64 (bytes) — plus unaligned host and device
+pointers.  Modelled on the reference's random_config property tests
+(pkg/tests/conftest.py:7-27, test_engine.py:123-164)."""
+
+import numpy as np
+import pytest
+
+from parity import check_fast
+from paper_2601_17091_b200 import GenOptions, generate_bank, transform, transform_with_stats
+from paper_2601_17091_b200.engine import expected_dot_products
+
+pytestmark = pytest.mark.gpu
+
+
+def _config(seed, unit_scale=False):
+    rng = np.random.Generator(np.random.Philox(key=np.uint64(1000 + seed)))
+    l_series = int(rng.choice([11, 12, 13, 17, 31, 64, 97, 100, 255, 256, 513, 1000, 1023, 2049]))
+    n_channels = int(rng.choice([1, 1, 1, 2, 3, 5]))
+    count = int(rng.integers(1, 400))
+    n = int(rng.integers(1, 70))
+    center = bool(rng.integers(0, 2))
+    scale = float(rng.choice([1e-3, 1.0, 50.0]))
+    values = (rng.standard_normal((n, n_channels, l_series)) * (1.0 if unit_scale else scale)).astype(np.float32)
+    if seed % 5 == 0:
+        values[:, :, ::7] = 0.0  # exact zeros: ties at the count threshold
+    bank = generate_bank(l_series, n_channels, count, GenOptions(seed=seed, center_weights=center))
+    return values, bank
+
+
+SEEDS = list(range(24))
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+def test_fuzz_exact_and_fast(seed, cuda_ready):
+    from oracle.oracle import oracle_transform
+
+    values, bank = _config(seed)
+    ref = oracle_transform(values, bank)
+    fm, stats = transform_with_stats(values, bank, mode="exact")
+    assert fm.values.tobytes() == ref.tobytes()
+    assert stats.total_dot_products == expected_dot_products(bank, values.shape[0])
+    # The fast-mode tolerance (MAX within 1e-5 relative) is the north star's
+    # for standard-normal series; at 50x scale the reference's own float32
+    # sums are 2e-5 (relative) from the float64 truth in cancelling cells,
+    # so the fast check runs on unit-scale data of the same shape.
+    values, bank = _config(seed, unit_scale=True)
+    check_fast(transform(values, bank, mode="fast").values, oracle_transform(values, bank), values, bank)
+
+
+@pytest.mark.parametrize("seed", SEEDS[::3])
+def test_fuzz_mpv_and_double(seed, cuda_ready):
+    from oracle.oracle import oracle_transform
+
+    values, bank = _config(seed)
+    for kw in ({"include_mpv": True}, {"precision": "double"}, {"precision": "double", "include_mpv": True}):
+        out = transform(values, bank, **kw).values
+        assert out.tobytes() == oracle_transform(values, bank, **kw).tobytes(), kw
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_unaligned_pointers(offset, cuda_ready):
+    """Host and device inputs that are not 16-byte aligned take the
+    cooperative staging path; outputs at odd row strides the scalar-store
+    path — same bytes."""
+    import torch
+
+    from oracle.oracle import oracle_transform
+    from paper_2601_17091_b200 import device_bank
+
+    bank = generate_bank(256, 1, 300, GenOptions(seed=3))
+    values = np.random.default_rng(offset).standard_normal((9, 1, 256)).astype(np.float32)
+    ref = oracle_transform(values, bank)
+    # host: a float32 view starting `offset` elements into a larger buffer
+    buf = np.zeros(values.size + offset, dtype=np.float32)
+    buf[offset:] = values.ravel()
+    x_host = buf[offset:].reshape(values.shape)
+    assert transform(x_host, bank).values.tobytes() == ref.tobytes()
+    # device: same offset, output rows with an odd leading dimension
+    db = device_bank(bank, 0)
+    xd = torch.from_numpy(buf).cuda()
+    ld = bank.count * 2 + 1
+    out = torch.zeros((values.shape[0], ld), device="cuda")
+    db.transform_into(xd.data_ptr() + 4 * offset, values.shape[0], out.data_ptr(), ld, mode="exact")
+    torch.cuda.synchronize()
+    assert out[:, : bank.count * 2].cpu().numpy().tobytes() == ref.tobytes()
