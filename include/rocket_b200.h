@@ -112,9 +112,11 @@ int rk_bank_info(rk_bank_t bank, rk_bank_info_t* info);
  * [row0, row0 + n_series) of out (same element type, row stride ld_out
  * elements) in the reference layout: out[row, k*fpk] = ppv_k,
  * out[row, k*fpk + 1] = max_k and, for fpk == 3, out[row, k*fpk + 2] = mpv_k
- * (features.py:1-5, engine.py:186-188, 236-247).  float32 with fpk == 2 runs
- * the FFMA2 kernels in either mode; float64 or fpk == 3 run the cell kernel
- * (the reference loop order, exact in both modes).  x and out may be host or
+ * (features.py:1-5, engine.py:186-188, 236-247).  float32 runs the FFMA2
+ * kernels in either mode, except fpk == 3 in RK_MODE_EXACT; float64, and
+ * fpk == 3 in RK_MODE_EXACT, run the cell kernels (the reference loop
+ * order, bit-identical).  Fast-mode MPV sums the positive outputs per lane
+ * and then across the warp (within 1e-5 relative).  x and out may be host or
  * device pointers.  stream is a
  * cudaStream_t (NULL = the library's per-device stream); for device x and
  * out the call is asynchronous on that stream, otherwise it returns after

@@ -19,33 +19,36 @@ void fill_class(rk::KernelFn* t, int cls) {
 }
 
 template <int RI, int P, int NC>
-void fill_wide(rk::WarpFn* wide, int cls) {
+void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   constexpr int R = rk::r_of(RI);
   wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false>;
-  if constexpr (RI <= rk::kExactRIdxCap) wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
+  if constexpr (RI <= rk::kExactRIdxCap) {
+    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false, true>;
+  }
 }
 
 template <int RI>
-void fill_r(rk::KernelFn* ct, rk::WarpFn* dt) {
+void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
   constexpr int R = rk::r_of(RI);
   const int base = (kLenIdx * rk::kNumR + RI) * rk::kNumNck;
   fill_class<RI, 0>(ct, base + 0);
   fill_class<RI, 1>(ct, base + 1);
   fill_class<RI, 3>(ct, base + 3);
   if constexpr (R == 1) fill_class<RI, 2>(ct, base + 2);  // generic channels: 1 position per lane
-  fill_wide<RI, 2, 1>(dt, base + 0);
-  fill_wide<RI, 1, 2>(dt, base + 1);
-  fill_wide<RI, 1, 1>(dt, base + 3);
+  fill_wide<RI, 2, 1>(dt, mt, base + 0);
+  fill_wide<RI, 1, 2>(dt, mt, base + 1);
+  fill_wide<RI, 1, 1>(dt, mt, base + 3);
 }
 }  // namespace
 
 #define RK_CAT2(a, b) a##b
 #define RK_CAT(a, b) RK_CAT2(a, b)
 
-void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt) {
-  fill_r<0>(ct, dt);
-  fill_r<1>(ct, dt);
-  fill_r<2>(ct, dt);
-  fill_r<3>(ct, dt);
-  fill_r<4>(ct, dt);
+void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
+  fill_r<0>(ct, dt, mt);
+  fill_r<1>(ct, dt, mt);
+  fill_r<2>(ct, dt, mt);
+  fill_r<3>(ct, dt, mt);
+  fill_r<4>(ct, dt, mt);
 }

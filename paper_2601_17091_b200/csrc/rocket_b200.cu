@@ -82,7 +82,9 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
   };
   // a masked step adds a compare and a select per last-tap load (the
   // NaN-slot masking, transform_kernel.cuh load_window_masked)
-  return nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) + 40 * G + 60;
+  static const int mpct = getenv("RK_MASK_COST_PCT") ? atoi(getenv("RK_MASK_COST_PCT")) : 100;
+  static const int chunk_extra = getenv("RK_CHUNK_COST") ? atoi(getenv("RK_CHUNK_COST")) : 60;
+  return nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) * mpct / 100 + 40 * G + chunk_extra;
 }
 
 }  // namespace
@@ -241,10 +243,11 @@ using rk::WarpFn;
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
   WarpFn dfn[2 * rk::kNumClasses] = {};
+  WarpFn mfn[rk::kNumClasses] = {};  // fast-mode MPV wide kernels
   KernelTable() {
-    rk_fill_tables_7(fn, dfn);
-    rk_fill_tables_9(fn, dfn);
-    rk_fill_tables_11(fn, dfn);
+    rk_fill_tables_7(fn, dfn, mfn);
+    rk_fill_tables_9(fn, dfn, mfn);
+    rk_fill_tables_11(fn, dfn, mfn);
   }
 };
 const KernelTable& kernel_table() {
@@ -352,7 +355,9 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
-    WarpFn fn = kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
+    // fpk 3 in fast mode: MPV kernels, R capped like exact mode (registers)
+    WarpFn fn = fpk == 3 ? kernel_table().mfn[exec_cls(wl.cls, 1)]
+                         : kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (const void*)fn, smem * spi);
     if (rc) return rc;
@@ -497,7 +502,10 @@ int launch_cells(rk_bank_t b, DeviceState* st, const void* d_x, int esz, int64_t
 int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_outv, int64_t ld_out, int fpk,
            int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters, int esz) {
   if (n <= 0) return RK_OK;
-  if (esz == 8 || fpk == 3) return launch_cells(b, st, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec, d_counters);
+  // float64, and MPV in exact mode (its ordered positive sum), run the cell
+  // kernels; fast-mode MPV runs the wide kernels with summed positives
+  if (esz == 8 || (fpk == 3 && (mode == RK_MODE_EXACT || !b->wide_path)))
+    return launch_cells(b, st, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec, d_counters);
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));

@@ -186,18 +186,25 @@ __device__ __forceinline__ void load_window_masked(float (&xw)[R + LEN - 1], con
 
 // Per-lane pooled state for the kernels of one chunk.  ext is the running
 // max (EXACT) or the running min of acc' = -(output) (FAST).
-template <int G>
+// MPV (FAST only) adds per-pair partial sums of min(acc', 0) = -(positive
+// outputs).
+template <int G, bool MPV = false>
 struct Pool {
   unsigned cnt[G];
   float ext[G];
+  float2 ps[MPV ? G / 2 : 1];
 };
 
-template <int G, bool EXACT>
-__device__ __forceinline__ void pool_init(Pool<G>& st) {
+template <int G, bool EXACT, bool MPV = false>
+__device__ __forceinline__ void pool_init(Pool<G, MPV>& st) {
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     st.cnt[g] = 0u;
     st.ext[g] = EXACT ? -INFINITY : INFINITY;
+  }
+  if (MPV) {
+#pragma unroll
+    for (int q = 0; q < G / 2; ++q) st.ps[q] = make_float2(0.0f, 0.0f);
   }
 }
 
@@ -239,9 +246,9 @@ __device__ __forceinline__ void pool_one(unsigned& cnt, float& ext, float a, flo
 
 // Pool R positions of P kernel pairs; position r is valid while
 // r*d < nleft (MASKED only).
-template <int R, int P, bool EXACT, bool MASKED>
-__device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)[P][R], const float (&thr)[2 * P],
-                                            bool live, int nleft, int d) {
+template <int R, int P, bool EXACT, bool MASKED, bool MPV = false>
+__device__ __forceinline__ void pool_update(Pool<2 * P, MPV>& st, const float2 (&acc)[P][R],
+                                            const float (&thr)[2 * P], bool live, int nleft, int d) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const bool ok = !MASKED || (live && (r * d < nleft));
@@ -249,6 +256,10 @@ __device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)
     for (int p = 0; p < P; ++p) {
       pool_one<EXACT, MASKED>(st.cnt[2 * p], st.ext[2 * p], acc[p][r].x, thr[2 * p], ok);
       pool_one<EXACT, MASKED>(st.cnt[2 * p + 1], st.ext[2 * p + 1], acc[p][r].y, thr[2 * p + 1], ok);
+      if (MPV) {
+        // min(NaN, 0) = 0: dead positions of masked steps add nothing
+        st.ps[p] = __fadd2_rn(st.ps[p], make_float2(fminf(acc[p][r].x, 0.0f), fminf(acc[p][r].y, 0.0f)));
+      }
     }
   }
 }
@@ -256,21 +267,28 @@ __device__ __forceinline__ void pool_update(Pool<2 * P>& st, const float2 (&acc)
 // Finish one chunk: reduce the per-lane pools over the warp; lane g
 // finishes kernel g: out[row, col*fpk] = ppv, out[row, col*fpk+1] = max
 // (engine.py:186-188).
-template <int G, bool EXACT, class CH>
-__device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __restrict__ orow, int fpk,
+template <int G, bool EXACT, class CH, bool MPV = false>
+__device__ __forceinline__ void finish_chunk(const CH& c, Pool<G, MPV>& st, float* __restrict__ orow, int fpk,
                                              int vec_out, int lane) {
   unsigned my_cnt = 0;
-  float my_ext = 0.0f, my_bias = 0.0f;
+  float my_ext = 0.0f, my_bias = 0.0f, my_ps = 0.0f;
   int my_col = 0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const unsigned tot = __reduce_add_sync(kFull, st.cnt[g]);
     const float e = EXACT ? warp_max(st.ext[g]) : warp_min(st.ext[g]);
+    float ps = 0.0f;
+    if (MPV) {
+      ps = (g & 1) ? st.ps[g / 2].y : st.ps[g / 2].x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(kFull, ps, o);
+    }
     if (lane == g) {
       my_cnt = tot;
       my_ext = e;
       my_bias = c.bias[g];
       my_col = c.col[g];
+      my_ps = ps;
     }
   }
   if (lane < c.nk) {
@@ -290,13 +308,16 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G>& st, float* __
       dst[0] = ppv;
       dst[1] = mx;
     }
+    // mpv = (sum of positive outputs) / count, divided in float64 like
+    // the reference (engine.py:244-247); 0 without positives
+    if (MPV) dst[2] = my_cnt ? __double2float_rn((double)(-my_ps) / (double)my_cnt) : 0.0f;
   }
 }
 
 // One step: R positions per lane (u0, u0+d, ..., u0+(R-1)d) for P kernel
 // pairs over NC channel slots.
-template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED>
-__device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (&chan)[NC],
+template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED, bool MPV = false>
+__device__ __forceinline__ void chunk_step(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                            const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                            const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
                                            const float* nan_slot) {
@@ -318,7 +339,7 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
     else
       accumulate<LEN, R, P, EXACT, false>(acc, w[s], xw, init_r, one2);
   }
-  pool_update<R, P, EXACT, false>(st, acc, thr, true, 0, d);
+  pool_update<R, P, EXACT, false, MPV>(st, acc, thr, true, 0, d);
 }
 
 // Lane map.  Positions v in [0, n) (centre u = lo + v) are split into runs
@@ -328,8 +349,8 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P>& st, const float* const (
 // all complete runs go through the unmasked path; the remaining starts
 // (an incomplete 32-group and the final partial run, whose positions
 // v0 + r*d may pass n) through masked steps with clamped reads.
-template <int LEN, int R, int P, int NC, bool EXACT>
-__device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* const (&chan)[NC],
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false>
+__device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
                                               int r32, float invd, const float* nan_slot, int lane) {
@@ -348,7 +369,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   const int dv = q32 * RD + r32;
 #pragma unroll(kStepUnroll)
   for (int stp = 0; stp < nfull; ++stp) {
-    chunk_step<LEN, R, P, NC, EXACT, false>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
+    chunk_step<LEN, R, P, NC, EXACT, false, MPV>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
     s += r32;
     v0 += dv;
     if (s >= d) {
@@ -358,7 +379,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P>& st, const float* cons
   }
   for (int base = nfull << 5; base < starts; base += 32) {
     const bool live = base + lane < starts;
-    chunk_step<LEN, R, P, NC, EXACT, true>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
+    chunk_step<LEN, R, P, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
                                            live ? n - v0 : 0, nan_slot);
     s += r32;
     v0 += dv;
@@ -858,7 +879,7 @@ __device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned 
                : "memory");
 }
 
-template <int LEN, int R, int P, int NC, bool EXACT>
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
@@ -937,11 +958,12 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         const float* chan[NC];
 #pragma unroll
         for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
-        Pool<2 * P> st;
-        pool_init<2 * P, EXACT>(st);
-        run_positions<LEN, R, P, NC, EXACT>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32, c.invd,
-                                            &s_nan, lane);
-        finish_chunk<2 * P, EXACT>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out, lane);
+        Pool<2 * P, MPV> st;
+        pool_init<2 * P, EXACT, MPV>(st);
+        run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32,
+                                                 c.invd, &s_nan, lane);
+        finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
+                                                p.h.vec_out, lane);
         done += (unsigned long long)c.nk * (unsigned long long)c.n;
       }
     }

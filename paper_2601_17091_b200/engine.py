@@ -13,8 +13,11 @@ Arithmetic modes (keyword-only ``mode``):
   "fast"            — FFMA2 with the bias folded in; within the north-star
                       tolerance (MAX 1e-5 relative, PPV exact except for
                       outputs within 1e-6 of zero).
-precision="double" and include_mpv=True run the cell kernel, which follows
-the reference loop order exactly in both modes (engine.py:193-249).
+precision="double" runs the cell kernels, which follow the reference loop
+order exactly in both modes; include_mpv=True does too in "exact" mode
+(the ordered positive sum, engine.py:193-249), while "fast" mode computes
+MPV in the FFMA2 kernels from per-lane sums of the positive outputs (MPV
+within 1e-5 relative, tests/parity.py).
 """
 
 import ctypes

@@ -49,6 +49,8 @@ def test_fuzz_exact_and_fast(seed, cuda_ready):
     # so the fast check runs on unit-scale data of the same shape.
     values, bank = _config(seed, unit_scale=True)
     check_fast(transform(values, bank, mode="fast").values, oracle_transform(values, bank), values, bank)
+    check_fast(transform(values, bank, mode="fast", include_mpv=True).values,
+               oracle_transform(values, bank, include_mpv=True), values, bank, fpk=3)
 
 
 @pytest.mark.parametrize("seed", SEEDS[::3])

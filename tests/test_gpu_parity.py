@@ -183,7 +183,9 @@ OTHER = [(name, v) for name, case in gc.CASES.items() for v in case["variants"] 
 
 @pytest.mark.parametrize("name,variant", OTHER)
 def test_double_and_mpv_bytes_match_reference(name, variant, golden_transforms, cuda_ready):
-    """precision="double" and include_mpv=True (the cell kernel) in both modes."""
+    """precision="double" (both modes) and include_mpv=True in exact mode run
+    the cell kernels: bytes equal.  Single-precision MPV in fast mode runs
+    the wide kernels: the fast tolerance, MPV included."""
     values, bank = _case(name)
     precision = variant.split("_")[0]
     mpv = variant.endswith("_mpv")
@@ -191,8 +193,23 @@ def test_double_and_mpv_bytes_match_reference(name, variant, golden_transforms, 
     for mode in ("exact", "fast"):
         fm, stats = transform_with_stats(values, bank, include_mpv=mpv, precision=precision, mode=mode)
         assert fm.values.dtype == ref.dtype and fm.values.shape == ref.shape
-        assert fm.values.tobytes() == ref.tobytes()
+        if mode == "fast" and mpv and precision == "single":
+            check_fast(fm.values, ref, values, bank, fpk=3)
+        else:
+            assert fm.values.tobytes() == ref.tobytes()
         assert stats.total_dot_products == int(golden_transforms[f"{name}/{variant}/executed"][0])
+
+
+def test_fast_mpv_config2_rows(cuda_ready):
+    """Fast-mode MPV (wide kernels) at the BASELINE shape: PPV/MAX within the
+    north-star tolerance, MPV within 1e-5 relative (certified cells aside)."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(1024, 1, 10000, GenOptions(seed=0))
+    values = synth_random(16, 1, 1024, seed=1).values
+    ref = oracle_transform(values, bank, include_mpv=True)
+    rep = check_fast(transform(values, bank, include_mpv=True, mode="fast").values, ref, values, bank, fpk=3)
+    assert rep["cells"] == 16 * 10000
 
 
 def test_mpv_and_double_config2_rows_vs_oracle(cuda_ready):
