@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--series", type=int, default=None, help="override series per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the MPV / float64 throughput lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -273,6 +274,29 @@ def main():
     other = "exact" if args.mode == "fast" else "fast"
     ms_other = timed(other)
 
+    # ---- the other feature sets, device-resident, on a 20k-series slice ----
+    variants = None
+    if not args.no_variants:
+        variants = {}
+        nv = min(n, 20000)
+        for name, fpk_v, prec, mode_v in (("mpv_fast", 3, "single", "fast"), ("mpv_exact", 3, "single", "exact"),
+                                          ("double", 2, "double", "exact")):
+            dt = torch.float64 if prec == "double" else torch.float32
+            xv = x_dev[:nv].to(dt).contiguous()
+            ov = torch.empty((nv, bank.count * fpk_v), device="cuda", dtype=dt)
+            db.transform_into(xv.data_ptr(), nv, ov.data_ptr(), bank.count * fpk_v, mode=mode_v, fpk=fpk_v,
+                              precision=prec, stream=sptr)
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            db.transform_into(xv.data_ptr(), nv, ov.data_ptr(), bank.count * fpk_v, mode=mode_v, fpk=fpk_v,
+                              precision=prec, stream=sptr)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            variants[name] = {"value": nv / (ev0.elapsed_time(ev1) / 1e3), "unit": "series/s", "series": nv,
+                              "fpk": fpk_v, "precision": prec, "mode": mode_v}
+            del xv, ov
+
     # ---- e2e through the public C-ABI call with pinned host buffers --------
     e2e = None
     if not args.no_e2e:
@@ -359,6 +383,7 @@ def main():
                            "value": total_series / (ms_other / 1e3),
                            "achieved_tflops": flops_series * n / (ms_other / args.steps / 1e3) / 1e12},
             "e2e": e2e,
+            "variants": variants,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "energy": energy,
