@@ -56,6 +56,10 @@ WANT = [
     "launch__grid_size", "launch__occupancy_limit_shared_mem", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smsp__inst_executed.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smsp__sass_inst_executed_op_shared_ld.sum",
+    "derived__memory_l1_conflicts_shared_nway", "derived__memory_l1_wavefronts_shared_excessive",
+    "smsp__sass_branch_targets_threads_divergent.sum", "smsp__sass_branch_targets.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
