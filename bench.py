@@ -373,6 +373,7 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_MEASURED, "traffic": traffic,
                          "flops_per_series": flops_series,
                          "algorithmic_bytes": (4 * cfg["c"] * cfg["l"] + 4 * fpk * bank.count) * n,
+                         "hbm_GBps": (traffic / (ms_step / 1e3) / 1e9) if traffic else None,
                          "traffic_source": "profiles/ncu_summary_%s.json (ncu dram bytes of one transform, "
                                            "scaled to this step's series)" % args.config if traffic else None,
                          "peak_source": "measured FFMA2 microbenchmark (profiles/r01_fp32_peak_microbench.jsonl); "
