@@ -850,7 +850,10 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 // CTAs x W is sized for 24 warps per SM (shared memory permitting).
 namespace rk {
 
-constexpr int kWideMaxWarps = 24;
+#ifndef RK_WIDE_WARPS
+#define RK_WIDE_WARPS 24  // resident warps per SM the wide kernel is built for (~80 registers)
+#endif
+constexpr int kWideMaxWarps = RK_WIDE_WARPS;
 
 // 1-D TMA (cp.async.bulk) staging of whole series rows, completed on an
 // mbarrier.
