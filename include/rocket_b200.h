@@ -177,7 +177,8 @@ int64_t rk_run_batch_f64(const double* x, int64_t n_instances,
  * pinned buffers) overlap batch by batch.  Non-finite inputs fail with
  * RK_ERR_INVALID, as engine._check_shapes does (engine.py:252-268), after
  * the rows before them were written.  batch_rows <= 0 picks a batch.
- * *executed (may be NULL) = positions_per_series * n_series. */
+ * *executed (may be NULL) receives the positions counted on the device
+ * (== positions_per_series * n_series). */
 int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset,
                         const void* x, int32_t in_dtype, int64_t n_series,
                         int32_t out_fd, int64_t out_offset, int32_t dtype,

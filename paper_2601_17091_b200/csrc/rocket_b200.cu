@@ -317,6 +317,16 @@ bool is_device_pointer(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// Host memory the driver can DMA directly (cudaHostAlloc / registered).
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
 // The class a launch executes: exact mode runs the largest-R class with the
 // R = 7 instantiation (same chunks, only positions per lane differ).
 int exec_cls(int cls, int exact) {
@@ -609,6 +619,15 @@ int rk_abi_version(void) { return RK_ABI_VERSION; }
 
 // shared with the streaming runtime (rocket_stream.cu)
 int rk_set_error(int code, const char* message) { return fail(code, "%s", message); }
+
+// The device counter rk_transform accumulates executed positions into for
+// device-pointer calls on `stream` (rk_internal.h).
+int rk_stream_counter(rk_bank_t b, void* stream, unsigned long long** counter) {
+  DeviceState* st = nullptr;
+  int rc = device_state(b->device, &st);
+  if (rc) return rc;
+  return stream_scratch(st, stream ? (cudaStream_t)stream : st->stream, counter);
+}
 
 const char* rk_last_error(void) { return g_last_error.c_str(); }
 
@@ -1012,8 +1031,13 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
     }
     return RK_OK;
   }
-  // Host buffers: row batches through a pooled worker's device buffers on
-  // three streams (see Worker).
+  // Pageable host buffers (numpy arrays): the pinned-ring pipeline, whose
+  // host copies run on several threads (the first touch of a fresh output
+  // array is the bottleneck otherwise).
+  if (!dx && !dout && (!is_pinned_host(x) || !is_pinned_host(out)) && !getenv("RK_NO_HOST_RING"))
+    return rk_stream_host(b, x, dtype, n, out, ld_out, row0, fpk, mode, executed);
+  // Pinned host buffers: row batches through a pooled worker's device
+  // buffers on three streams (see Worker).
   Worker* w = nullptr;
   rc = acquire_worker(st, &w);
   if (rc) return rc;

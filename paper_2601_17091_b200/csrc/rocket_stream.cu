@@ -28,6 +28,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -50,6 +51,8 @@ struct Ring {
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t h2d_done[kSlots] = {}, d2h_done[kSlots] = {};
   cudaEvent_t in_ready[kDev] = {}, in_free[kDev] = {}, out_ready[kDev] = {}, out_free[kDev] = {};
+  unsigned long long* h_exec = nullptr;  // pinned: executed positions per batch
+  int64_t exec_cap = 0;
 };
 
 std::mutex g_ring_mu;
@@ -88,6 +91,9 @@ int ring_create(int device, Ring** out) {
 }
 
 void ring_free_buffers(Ring* r) {
+  if (r->h_exec) cudaFreeHost(r->h_exec);
+  r->h_exec = nullptr;
+  r->exec_cap = 0;
   for (int i = 0; i < kSlots; ++i) {
     if (r->h_in[i]) cudaFreeHost(r->h_in[i]);
     if (r->h_out[i]) cudaFreeHost(r->h_out[i]);
@@ -250,26 +256,54 @@ extern "C" void rk_stream_release(void) {
   g_free_rings.clear();
 }
 
-extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset, const void* x,
-                                   int32_t in_dtype, int64_t n, int32_t out_fd, int64_t out_offset,
-                                   int32_t dtype, int32_t fpk, int32_t mode, int64_t batch_rows,
-                                   int64_t* executed) {
-  if (executed) *executed = 0;
+namespace {
+
+// Copy `rows` rows of `row_bytes` from src (stride src_ld) to dst (stride
+// dst_ld) with up to `threads` threads: the destination is usually fresh
+// pageable memory, and its first-touch page faults are what bounds the copy,
+// so they are taken in parallel.
+void copy_rows(char* dst, int64_t dst_ld, const char* src, int64_t src_ld, int64_t row_bytes, int64_t rows,
+               int threads) {
+  const int64_t total = rows * row_bytes;
+  auto part = [&](int64_t r0, int64_t r1) {
+    if (dst_ld == row_bytes && src_ld == row_bytes) {
+      std::memcpy(dst + r0 * row_bytes, src + r0 * row_bytes, (size_t)((r1 - r0) * row_bytes));
+    } else {
+      for (int64_t r = r0; r < r1; ++r) std::memcpy(dst + r * dst_ld, src + r * src_ld, (size_t)row_bytes);
+    }
+  };
+  const int t = (int)std::max<int64_t>(1, std::min<int64_t>(threads, total / (4 << 20)));
+  if (t <= 1 || rows < t) {
+    part(0, rows);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int i = 0; i < t; ++i) pool.emplace_back(part, rows * i / t, rows * (i + 1) / t);
+  for (auto& th : pool) th.join();
+}
+
+// Where the rows come from and where the features go.
+struct StreamIO {
+  int in_fd = -1;             // source file (or -1: memory)
+  int64_t in_offset = 0;
+  const char* x = nullptr;    // source rows in memory (in_fd < 0)
+  int in_dtype = RK_DTYPE_F32;
+  bool check_finite = true;   // the reference's _check_shapes scan
+  int out_fd = -1;            // sink file (or -1: memory)
+  int64_t out_offset = 0;
+  char* out = nullptr;        // sink rows in memory (out_fd < 0)
+  int64_t out_ld_bytes = 0;   // sink row stride (memory)
+  int copy_threads = 1;
+};
+
+int run_stream(rk_bank_t bank, const StreamIO& io, int64_t n, int32_t dtype, int32_t fpk, int32_t mode,
+               int64_t batch_rows, int64_t* executed) {
   rk_bank_info_t info;
   int rc = rk_bank_info(bank, &info);
   if (rc) return rc;
-  if (n < 0) return rk_set_error(RK_ERR_INVALID, "n_series must be non-negative");
-  if (in_fd < 0 && !x && n > 0) return rk_set_error(RK_ERR_INVALID, "no input: in_fd < 0 and x is NULL");
-  if (out_fd < 0) return rk_set_error(RK_ERR_INVALID, "out_fd must be an open file descriptor");
-  if (in_offset < 0 || out_offset < 0) return rk_set_error(RK_ERR_INVALID, "negative file offset");
-  if ((in_dtype != RK_DTYPE_F32 && in_dtype != RK_DTYPE_F64) || (dtype != RK_DTYPE_F32 && dtype != RK_DTYPE_F64))
-    return rk_set_error(RK_ERR_INVALID, "unknown dtype");
-  if (fpk != 2 && fpk != 3) return rk_set_error(RK_ERR_INVALID, "features_per_kernel must be 2 or 3");
-  if (mode != RK_MODE_EXACT && mode != RK_MODE_FAST) return rk_set_error(RK_ERR_INVALID, "unknown mode");
   if (n == 0) return RK_OK;
-
   const int64_t row_vals = (int64_t)info.n_channels * info.l_series;
-  const int in_esz = in_dtype == RK_DTYPE_F64 ? 8 : 4;
+  const int in_esz = io.in_dtype == RK_DTYPE_F64 ? 8 : 4;
   const int esz = dtype == RK_DTYPE_F64 ? 8 : 4;
   const int64_t in_row = row_vals * in_esz;   // bytes per row in the source
   const int64_t dev_row = row_vals * esz;     // bytes per row on the device
@@ -277,9 +311,10 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
   const int64_t out_row = out_cols * esz;
   int64_t batch = batch_rows;
   if (batch <= 0) {
-    // ~512 MB of features per batch, but never so few series that the
-    // transform kernel runs below a full wave of CTAs
-    batch = std::max<int64_t>(4096, ((int64_t)512 << 20) / std::max<int64_t>(1, out_row));
+    // ~256 MB of features per batch (RK_STREAM_BATCH_MB), but never so few
+    // series that the transform kernels run below a full wave of CTAs
+    static const int64_t mb = getenv("RK_STREAM_BATCH_MB") ? std::max(1, atoi(getenv("RK_STREAM_BATCH_MB"))) : 256;
+    batch = std::max<int64_t>(4096, (mb << 20) / std::max<int64_t>(1, out_row));
     batch = std::min<int64_t>(batch, 65535);
   }
   batch = std::min(batch, n);
@@ -308,6 +343,16 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
   } give_back{ring};
   rc = ring_reserve(ring, (size_t)(batch * dev_row), (size_t)(batch * out_row));
   if (rc) return rc;
+  if (ring->exec_cap < nb) {
+    if (ring->h_exec) cudaFreeHost(ring->h_exec);
+    ring->h_exec = nullptr;
+    ST_CUDA(cudaHostAlloc(&ring->h_exec, sizeof(unsigned long long) * nb, cudaHostAllocDefault));
+    ring->exec_cap = nb;
+  }
+  // the kernels count executed positions on the device, per batch
+  unsigned long long* d_exec = nullptr;
+  rc = rk_stream_counter(bank, (void*)ring->comp, &d_exec);
+  if (rc) return rc;
 
   Progress pg;
   auto rows_of = [&](int64_t k) { return std::min(batch, n - k * batch); };
@@ -333,23 +378,25 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
         src_buf = staging.data();
       }
       std::string why;
-      if (in_fd >= 0) {
-        if (!read_full(in_fd, src_buf, src_bytes, in_offset + r0 * in_row, &why)) {
+      if (io.in_fd >= 0) {
+        if (!read_full(io.in_fd, src_buf, src_bytes, io.in_offset + r0 * in_row, &why)) {
           pg.error(RK_ERR_INVALID, why);
           return;
         }
       } else {
-        std::memcpy(src_buf, static_cast<const char*>(x) + r0 * in_row, src_bytes);
+        std::memcpy(src_buf, io.x + r0 * in_row, src_bytes);
       }
       const int64_t count = rows * row_vals;
-      const int64_t bad = in_esz == 8 ? first_nonfinite<uint64_t, 0x7ff0000000000000ull>(src_buf, count)
-                                      : first_nonfinite<uint32_t, 0x7f800000u>(src_buf, count);
-      if (bad >= 0) {
-        char buf[160];
-        snprintf(buf, sizeof(buf), "input contains non-finite values (series %lld)",
-                 (long long)(r0 + bad / row_vals));
-        pg.error(RK_ERR_INVALID, buf);
-        return;
+      if (io.check_finite) {
+        const int64_t bad = in_esz == 8 ? first_nonfinite<uint64_t, 0x7ff0000000000000ull>(src_buf, count)
+                                        : first_nonfinite<uint32_t, 0x7f800000u>(src_buf, count);
+        if (bad >= 0) {
+          char buf[160];
+          snprintf(buf, sizeof(buf), "input contains non-finite values (series %lld)",
+                   (long long)(r0 + bad / row_vals));
+          pg.error(RK_ERR_INVALID, buf);
+          return;
+        }
       }
       if (in_esz != esz) {
         if (in_esz == 8) {
@@ -375,11 +422,17 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
         pg.error(RK_ERR_CUDA, "cudaEventSynchronize(d2h) failed");
         return;
       }
-      std::string why;
-      if (!write_full(out_fd, ring->h_out[s], (size_t)(rows_of(k) * out_row), out_offset + k * batch * out_row,
-                      &why)) {
-        pg.error(RK_ERR_INVALID, why);
-        return;
+      const int64_t rows = rows_of(k);
+      if (io.out_fd >= 0) {
+        std::string why;
+        if (!write_full(io.out_fd, ring->h_out[s], (size_t)(rows * out_row), io.out_offset + k * batch * out_row,
+                        &why)) {
+          pg.error(RK_ERR_INVALID, why);
+          return;
+        }
+      } else {
+        copy_rows(io.out + k * batch * io.out_ld_bytes, io.out_ld_bytes, static_cast<const char*>(ring->h_out[s]),
+                  out_row, out_row, rows, io.copy_threads);
       }
       pg.set(&Progress::written, k + 1);
     }
@@ -402,6 +455,8 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
       const int trc = rk_transform(bank, ring->d_in[db], dtype, rows, ring->d_out[db], out_cols, 0, fpk, mode,
                                    (void*)ring->comp, nullptr);
       if (trc) return trc;
+      ST_CUDA(cudaMemcpyAsync(ring->h_exec + k, d_exec, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              ring->comp));
       ST_CUDA(cudaEventRecord(ring->in_free[db], ring->comp));
       ST_CUDA(cudaEventRecord(ring->out_ready[db], ring->comp));
       if (k >= kSlots && !pg.wait_past(&Progress::written, k - kSlots)) return RK_OK;
@@ -423,6 +478,64 @@ extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_off
   cudaStreamSynchronize(ring->comp);
   cudaStreamSynchronize(ring->d2h);
   if (pg.code != RK_OK) return rk_set_error(pg.code, pg.message.c_str());
-  if (executed) *executed = info.positions_per_series * n;
+  if (executed) {
+    int64_t tot = 0;
+    for (int64_t k = 0; k < nb; ++k) tot += (int64_t)ring->h_exec[k];
+    *executed = tot;
+  }
   return RK_OK;
+}
+
+int validate_common(int32_t in_dtype, int32_t dtype, int32_t fpk, int32_t mode, int64_t n) {
+  if (n < 0) return rk_set_error(RK_ERR_INVALID, "n_series must be non-negative");
+  if ((in_dtype != RK_DTYPE_F32 && in_dtype != RK_DTYPE_F64) || (dtype != RK_DTYPE_F32 && dtype != RK_DTYPE_F64))
+    return rk_set_error(RK_ERR_INVALID, "unknown dtype");
+  if (fpk != 2 && fpk != 3) return rk_set_error(RK_ERR_INVALID, "features_per_kernel must be 2 or 3");
+  if (mode != RK_MODE_EXACT && mode != RK_MODE_FAST) return rk_set_error(RK_ERR_INVALID, "unknown mode");
+  return RK_OK;
+}
+
+}  // namespace
+
+extern "C" int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset, const void* x,
+                                   int32_t in_dtype, int64_t n, int32_t out_fd, int64_t out_offset,
+                                   int32_t dtype, int32_t fpk, int32_t mode, int64_t batch_rows,
+                                   int64_t* executed) {
+  if (executed) *executed = 0;
+  rk_bank_info_t info;
+  int rc = rk_bank_info(bank, &info);
+  if (rc) return rc;
+  rc = validate_common(in_dtype, dtype, fpk, mode, n);
+  if (rc) return rc;
+  if (in_fd < 0 && !x && n > 0) return rk_set_error(RK_ERR_INVALID, "no input: in_fd < 0 and x is NULL");
+  if (out_fd < 0) return rk_set_error(RK_ERR_INVALID, "out_fd must be an open file descriptor");
+  if (in_offset < 0 || out_offset < 0) return rk_set_error(RK_ERR_INVALID, "negative file offset");
+  StreamIO io;
+  io.in_fd = in_fd;
+  io.in_offset = in_offset;
+  io.x = static_cast<const char*>(x);
+  io.in_dtype = in_dtype;
+  io.check_finite = true;
+  io.out_fd = out_fd;
+  io.out_offset = out_offset;
+  return run_stream(bank, io, n, dtype, fpk, mode, batch_rows, executed);
+}
+
+// rk_transform's path for pageable host buffers (rk_internal.h).
+extern "C" int rk_stream_host(rk_bank_t bank, const void* x, int32_t dtype, int64_t n, void* out, int64_t ld_out,
+                              int64_t row0, int32_t fpk, int32_t mode, int64_t* executed) {
+  if (executed) *executed = 0;
+  int rc = validate_common(dtype, dtype, fpk, mode, n);
+  if (rc) return rc;
+  const int esz = dtype == RK_DTYPE_F64 ? 8 : 4;
+  StreamIO io;
+  io.x = static_cast<const char*>(x);
+  io.in_dtype = dtype;
+  io.check_finite = false;  // the caller validated (engine._check_shapes)
+  io.out = static_cast<char*>(out) + row0 * ld_out * esz;
+  io.out_ld_bytes = ld_out * esz;
+  const unsigned hw = std::thread::hardware_concurrency();
+  io.copy_threads = (int)std::max(1u, std::min(16u, hw ? hw : 4u));
+  if (getenv("RK_COPY_THREADS")) io.copy_threads = std::max(1, atoi(getenv("RK_COPY_THREADS")));
+  return run_stream(bank, io, n, dtype, fpk, mode, 0, executed);
 }
