@@ -232,14 +232,8 @@ __device__ __forceinline__ void pool_one(unsigned& cnt, float& ext, float a, flo
       if (ok) cnt += __float_as_uint(a) >> 31;
       ext = ok ? fminf(ext, a) : ext;
     } else {
-#ifndef RK_ABL_NOCOUNT
       cnt += __float_as_uint(a) >> 31;
-#else
-      cnt ^= __float_as_uint(a) & 1u;
-#endif
-#ifndef RK_ABL_NOMIN
       ext = fminf(ext, a);
-#endif
     }
   }
 }
