@@ -74,6 +74,23 @@ def test_run_batch_dropin_signature(golden_transforms, cuda_ready):
     assert out[3:].tobytes() == golden_transforms["rc7/single"].tobytes()
 
 
+def test_run_batch_mpv_dropin(golden_transforms, cuda_ready):
+    """fpk = 3 through rk_run_batch_f32: _run_batch_mpv's bytes."""
+    lib = cuda_ready
+    values, bank = _case("small")
+    x = np.ascontiguousarray(values, dtype=np.float32)
+    out = np.empty((x.shape[0], bank.count * 3), dtype=np.float32)
+    arrs = [np.ascontiguousarray(v) for v in (
+        bank.lengths, bank.dilations, bank.paddings, bank.biases.astype(np.float32),
+        bank.weights.astype(np.float32), bank.weight_offsets, bank.channel_indices, bank.channel_offsets,
+        bank.channel_counts)]
+    p = lambda arr: arr.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    executed = lib.rk_run_batch_f32(p(x), x.shape[0], x.shape[1], x.shape[2], *[p(a) for a in arrs],
+                                    bank.count, 1024, 3, p(out), out.shape[1], 0)
+    assert executed == expected_dot_products(bank, x.shape[0])
+    assert out.tobytes() == golden_transforms["small/single_mpv"].tobytes()
+
+
 def test_sharding_and_batching_are_pure_partitions(cuda_ready):
     values, bank = _case("rc300")
     whole = transform(values, bank)
