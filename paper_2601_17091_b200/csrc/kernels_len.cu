@@ -38,6 +38,7 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
   if constexpr (R == 1) fill_class<RI, 2>(ct, base + 2);  // generic channels: 1 position per lane
   fill_wide<RI, 2, 1>(dt, mt, base + 0);
   fill_wide<RI, 1, 2>(dt, mt, base + 1);
+  fill_wide<RI, 1, 0>(dt, mt, base + 2);
   fill_wide<RI, 1, 1>(dt, mt, base + 3);
 }
 }  // namespace

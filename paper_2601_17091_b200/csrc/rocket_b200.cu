@@ -50,7 +50,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 // per-call device scratch: the executed counter + one item counter per class
-constexpr int kMaxLaunches = 1024;
+constexpr int kMaxLaunches = 4096;
 constexpr size_t kScratchBytes = sizeof(unsigned long long) + sizeof(int) * kMaxLaunches;
 
 constexpr int kLenIdx[12] = {-1, -1, -1, -1, -1, -1, -1, 0, -1, 1, -1, 2};
@@ -64,7 +64,7 @@ struct HostChunk {
 // (positions per lane, stride = dilation), following the kernel's lane map
 // (run_positions): full 32-lane steps of R positions, then 1-position
 // masked steps for the leftover positions.
-int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
+int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false) {
   const int64_t G = 2 * P;
   const int64_t RD = (int64_t)R * d;
   const int64_t A = n / RD;
@@ -78,6 +78,7 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R) {
            + r * G * 2                   // count (FSETP + IADD)
            + (r * G + 1) / 2             // max (FMNMX3 pairs)
            + 2 * (r + len - 1) * nc      // window loads + addresses
+           + (dyn ? (P * len + 8) * nc : 0)  // run-time slots: weight reloads, slot loop
            + extra;
   };
   // a masked step adds a compare and a select per last-tap load (the
@@ -372,7 +373,7 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     int rc = set_kernel_smem(st, (const void*)fn, smem * spi);
     if (rc) return rc;
     const int nck = wl.cls % rk::kNumNck;
-    const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
+    const int P = rk::nck_pairs(nck), NC = std::max(1, rk::nck_slots(nck));
     const int len = c_len(wl.cls);
     rk::WHeader& h = params.h;
     h.x = d_x;
@@ -727,6 +728,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   b->positions = positions;
   b->useful_flops = flops;
 
+  // every chunk class runs on the wide kernel unless RK_NO_WIDE_PATH asks
+  // for the class kernel (diagnostics)
+  const bool wide_ok = !getenv("RK_NO_WIDE_PATH");
   std::vector<float> wpack;
   std::vector<int> chan_off;
   for (auto& kv : groups) {
@@ -741,7 +745,12 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     while (k0 < ks.size()) {
       const size_t left = ks.size() - k0;
       // 1-channel groups: 4-kernel chunks (2 FFMA2 pairs), 1-pair chunks
-      // for a remainder of 1 or 2; multichannel: 1 pair per chunk.
+      // for a remainder of 1 or 2; 2-channel groups: 1 pair per chunk (both
+      // slots' weights in uniform registers); >= 3 channels: 1 pair per
+      // chunk with the run-time slot loop (1 position per lane on the
+      // class-kernel path).  Measured: 2 pairs with the slot loop (R <= 5
+      // for registers) is slower both for 2 channels (-38 % at config 5) and
+      // for 3+ (-17 % at C = 4).
       int P, nck;
       if (nc == 1) {
         P = left >= 3 ? 2 : 1;
@@ -769,8 +778,8 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       int best_r = 0;
       int64_t best = INT64_MAX;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
-        if (nck == 2 && ri != 0) continue;  // generic path is 1 position per lane
-        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri));
+        if (nck == 2 && !wide_ok && ri != 0) continue;  // class-kernel generic path: 1 position per lane
+        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), rk::nck_slots(nck) == 0);
         if (cst < best) {
           best = cst;
           best_r = ri;
@@ -842,30 +851,41 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
     const int by_smem = (int)((st->smem_optin + 1024) / per_cta);
-    bool no_generic = true;
-    for (auto& hc : b->chunks) no_generic = no_generic && (hc.dev.cls % rk::kNumNck) != 2;
     const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6;
-    if (no_generic && by_smem >= 1 && !getenv("RK_NO_WIDE_PATH")) {
+    if (by_smem >= 1 && wide_ok) {
       b->wide_path = true;
       b->wide_ctas_smem = by_smem;
       b->wide_ctas_per_sm = std::min(by_smem, cap);
+      const int blob_bytes = rk::kBlobFloat4 * 16;
       for (int cls = 0; cls < rk::kNumClasses; ++cls) {
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
         const int nck = cls % rk::kNumNck;
-        const int P = nck == 0 ? 2 : 1, NC = nck == 1 ? 2 : 1;
+        const int P = rk::nck_pairs(nck), NC = rk::nck_slots(nck);
         const int len = 7 + 2 * (cls / (rk::kNumNck * rk::kNumR));
-        const int wbytes = NC * P * len * 8;
-        const int per_chunk = (int)sizeof(rk::WChunk) + wbytes;
-        const int cap = (rk::kBlobFloat4 * 16) / per_chunk;
-        for (int i0 = cb; i0 < ce; i0 += cap) {
-          const int nch = std::min(cap, ce - i0);
+        // bytes after the descriptor: fixed slots -> the weights; run-time
+        // slots -> the weights then the slot list (16-byte aligned)
+        auto data_bytes = [&](const rk::DevChunk& c) {
+          return NC ? NC * P * len * 8 : c.nc * P * len * 8 + ((c.nc * 4 + 15) / 16) * 16;
+        };
+        int i0 = cb;
+        while (i0 < ce) {
+          int nch = 0, used = 0;
+          while (i0 + nch < ce) {
+            const int add = (int)sizeof(rk::WChunk) + data_bytes(b->chunks[i0 + nch].dev);
+            if (used + add > blob_bytes) break;
+            used += add;
+            ++nch;
+          }
+          if (nch == 0) return fail(RK_ERR_CAPACITY, "a chunk's weights exceed the kernel parameter block");
           rk_bank_s::WideLaunch wl;
           wl.cls = cls;
           wl.n_chunks = nch;
           wl.dense_flops = 0;
           wl.blob.assign(rk::kBlobFloat4, rk::float4_t{0, 0, 0, 0});
           char* raw = reinterpret_cast<char*>(wl.blob.data());
+          std::vector<std::pair<int, int>> wranges;  // float ranges holding weights (negated for fast mode)
+          int cursor = nch * (int)sizeof(rk::WChunk);
           for (int j = 0; j < nch; ++j) {
             const rk::DevChunk& c = b->chunks[i0 + j].dev;
             rk::WChunk wc;
@@ -879,22 +899,35 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
               wc.bias[g] = c.bias[g];
               wc.thr[g] = c.thr[g];
             }
-            for (int s2 = 0; s2 < NC; ++s2) wc.ch[s2] = chan_off[c.chofs + s2] / (int)sstride;
+            const int wbytes = c.nc * P * len * 8;
+            if (NC) {
+              for (int s2 = 0; s2 < NC; ++s2) wc.ch[s2] = chan_off[c.chofs + s2] / (int)sstride;
+            } else {
+              wc.ch[0] = cursor;
+              wc.ch[1] = c.nc;
+            }
             wc.q32 = (short)c.q32;
             wc.r32 = (short)c.r32;
             wc.invd = c.invd;
             std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
-            std::memcpy(raw + (size_t)nch * sizeof(rk::WChunk) + (size_t)j * wbytes, wpack.data() + c.wofs, wbytes);
+            std::memcpy(raw + cursor, wpack.data() + c.wofs, wbytes);
+            wranges.emplace_back(cursor / 4, wbytes / 4);
+            if (!NC) {
+              int* slots = reinterpret_cast<int*>(raw + cursor + wbytes);
+              for (int s2 = 0; s2 < c.nc; ++s2) slots[s2] = chan_off[c.chofs + s2] / (int)sstride;
+            }
+            cursor += data_bytes(c);
             wl.dense_flops += (int64_t)2 * c.nk * c.nc * c.len * c.n;
           }
           // fast mode computes acc' = -b + sum (-w) x; (-w) * x == w * (-x)
           // bit for bit, so negating the weights replaces negating the
           // staged series and lets the rows be bulk-copied unchanged
           wl.blob_fast = wl.blob;
-          float* wf = reinterpret_cast<float*>(reinterpret_cast<char*>(wl.blob_fast.data()) +
-                                               (size_t)nch * sizeof(rk::WChunk));
-          for (size_t q = 0; q < (size_t)nch * wbytes / sizeof(float); ++q) wf[q] = -wf[q];
+          float* wf = reinterpret_cast<float*>(wl.blob_fast.data());
+          for (const auto& r : wranges)
+            for (int q = 0; q < r.second; ++q) wf[r.first + q] = -wf[r.first + q];
           b->wide_launches.push_back(std::move(wl));
+          i0 += nch;
         }
       }
       if ((int)b->wide_launches.size() > kMaxLaunches) {

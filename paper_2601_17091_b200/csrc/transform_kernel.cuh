@@ -60,7 +60,9 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // Class encoding: cls = ((len_idx * kNumR) + r_idx) * kNumNck + nc_kind
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
-//           2: >= 3 channels (generic); 3: 1 channel, 1 pair
+//           2: >= 3 channels, 1 pair (wide kernel: channel slots looped at
+//              run time; class kernel: the generic 1-position path);
+//           3: 1 channel, 1 pair
 constexpr int kNumR = 5;
 // positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX (odd: spreads lanes
 // over the shared-memory banks).  Exact-mode launches run the RK_RMAX class
@@ -68,6 +70,9 @@ constexpr int kNumR = 5;
 __host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 4 ? RK_RMAX : 2 * r_idx + 1; }
 constexpr int kExactRIdxCap = 3;
 constexpr int kNumNck = 4;
+// (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop
+__host__ __device__ constexpr int nck_pairs(int nck) { return nck == 0 ? 2 : 1; }
+__host__ __device__ constexpr int nck_slots(int nck) { return nck == 1 ? 2 : nck == 2 ? 0 : 1; }
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
 // One chunk (class-kernel layout, global memory).
@@ -375,6 +380,89 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
     const bool live = base + lane < starts;
     chunk_step<LEN, R, P, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
                                            live ? n - v0 : 0, nan_slot);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
+    }
+  }
+}
+
+// Run-time channel slots (NC = 0 kernels): the chunk's slot list and its
+// weights ([slot][pair][tap] float2) live in the launch's parameter block;
+// each step walks the slots in order — the reference's channel order — with
+// one slot's weights loaded at a time (uniform registers) and one window.
+template <int LEN, int R, int P, bool EXACT, bool MASKED, bool MPV = false>
+__device__ __forceinline__ void chunk_step_dyn(Pool<2 * P, MPV>& st, const float* sx, const int* slots, int nc,
+                                               const float2* wp, int S, const float (&thr)[2 * P],
+                                               const float2 (&init)[P], float2 one2, int u0, int d, int nleft,
+                                               const float* nan_slot) {
+  float2 init_r[P][R];
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int r = 0; r < R; ++r) init_r[p][r] = init[p];
+  float2 acc[P][R];
+  {
+    float xw[R + LEN - 1];
+    if (MASKED)
+      load_window_masked<LEN, R>(xw, sx + slots[0] * S, u0, d, nleft, nan_slot);
+    else
+      load_window<LEN, R>(xw, sx + slots[0] * S, u0, d);
+    float2 w[P][LEN];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int j = 0; j < LEN; ++j) w[q][j] = wp[q * LEN + j];
+    accumulate<LEN, R, P, EXACT, true>(acc, w, xw, init_r, one2);
+  }
+  for (int s = 1; s < nc; ++s) {
+    float xw[R + LEN - 1];
+    if (MASKED)
+      load_window_masked<LEN, R>(xw, sx + slots[s] * S, u0, d, nleft, nan_slot);
+    else
+      load_window<LEN, R>(xw, sx + slots[s] * S, u0, d);
+    float2 w[P][LEN];
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int j = 0; j < LEN; ++j) w[q][j] = wp[(s * P + q) * LEN + j];
+    accumulate<LEN, R, P, EXACT, false>(acc, w, xw, init_r, one2);
+  }
+  pool_update<R, P, EXACT, false, MPV>(st, acc, thr, true, 0, d);
+}
+
+// run_positions for run-time channel slots (same lane map).
+template <int LEN, int R, int P, bool EXACT, bool MPV = false>
+__device__ __forceinline__ void run_positions_dyn(Pool<2 * P, MPV>& st, const float* sx, const int* slots, int nc,
+                                                  const float2* wp, int S, const float (&thr)[2 * P],
+                                                  const float2 (&init)[P], float2 one2, int lo, int n, int d,
+                                                  int q32, int r32, float invd, const float* nan_slot, int lane) {
+  const int RD = R * d;
+  const int A = n / RD;
+  const int rem = n - A * RD;
+  const int full_starts = A * d;
+  const int starts = full_starts + min(d, rem);
+  const int nfull = full_starts >> 5;
+  int a = (int)((lane + 0.5f) * invd);
+  int s = lane - a * d;
+  int v0 = a * RD + s;
+  const int dv = q32 * RD + r32;
+  for (int stp = 0; stp < nfull; ++stp) {
+    chunk_step_dyn<LEN, R, P, EXACT, false, MPV>(st, sx, slots, nc, wp, S, thr, init, one2, lo + v0, d, n,
+                                                 nan_slot);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
+    }
+  }
+  for (int base = nfull << 5; base < starts; base += 32) {
+    const bool live = base + lane < starts;
+    chunk_step_dyn<LEN, R, P, EXACT, true, MPV>(st, sx, slots, nc, wp, S, thr, init, one2, lo + (live ? v0 : 0), d,
+                                                live ? n - v0 : 0, nan_slot);
     s += r32;
     v0 += dv;
     if (s >= d) {
@@ -938,30 +1026,47 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
       ci = __reduce_max_sync(kFull, __shfl_sync(kFull, ci, 0));
       if (ci >= p.h.n_chunks) break;
       const WChunk& c = chunks[ci];
-      const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
-      float2 w[NC][P][LEN];
-#pragma unroll
-      for (int s = 0; s < NC; ++s)
-#pragma unroll
-        for (int q = 0; q < P; ++q)
-#pragma unroll
-          for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
       float thr[2 * P];
       float2 init[P];
       chunk_consts<P, EXACT>(c, thr, init);
-      // the chunk's weights serve every staged series of the item
-      for (int si = 0; si < ns; ++si) {
-        const float* sx = smem + si * slot + H;
-        const float* chan[NC];
+      if constexpr (NC == 0) {
+        // run-time slots: ch[0] = byte offset of the chunk's weights in the
+        // block, ch[1] = slot count; the slot list follows the weights
+        const int nc = c.ch[1];
+        const float2* wp = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(p.blob) + c.ch[0]);
+        const int* slots = reinterpret_cast<const int*>(wp + nc * P * LEN);
+        for (int si = 0; si < ns; ++si) {
+          Pool<2 * P, MPV> st;
+          pool_init<2 * P, EXACT, MPV>(st);
+          run_positions_dyn<LEN, R, P, EXACT, MPV>(st, smem + si * slot + H, slots, nc, wp, S, thr, init, one2,
+                                                   c.lo, c.n, c.d, c.q32, c.r32, c.invd, &s_nan, lane);
+          finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
+                                                  p.h.vec_out, lane);
+          done += (unsigned long long)c.nk * (unsigned long long)c.n;
+        }
+      } else {
+        const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
+        float2 w[NC][P][LEN];
 #pragma unroll
-        for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
-        Pool<2 * P, MPV> st;
-        pool_init<2 * P, EXACT, MPV>(st);
-        run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32,
-                                                 c.invd, &s_nan, lane);
-        finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
-                                                p.h.vec_out, lane);
-        done += (unsigned long long)c.nk * (unsigned long long)c.n;
+        for (int s = 0; s < NC; ++s)
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+#pragma unroll
+            for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
+        // the chunk's weights serve every staged series of the item
+        for (int si = 0; si < ns; ++si) {
+          const float* sx = smem + si * slot + H;
+          const float* chan[NC];
+#pragma unroll
+          for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+          Pool<2 * P, MPV> st;
+          pool_init<2 * P, EXACT, MPV>(st);
+          run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32,
+                                                   c.invd, &s_nan, lane);
+          finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
+                                                  p.h.vec_out, lane);
+          done += (unsigned long long)c.nk * (unsigned long long)c.n;
+        }
       }
     }
   }

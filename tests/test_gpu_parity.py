@@ -286,3 +286,16 @@ def test_run_batch_f64_dropin(golden_transforms, cuda_ready):
     )
     assert executed == expected_dot_products(bank, x.shape[0])
     assert out.tobytes() == golden_transforms["rc5/double"].tobytes()
+
+
+def test_class_kernel_path_still_exact(cuda_ready, monkeypatch):
+    """RK_NO_WIDE_PATH (read when the device bank is built) runs every chunk
+    on the class kernel, including the 1-position generic path for 3+
+    channel slots: same bytes as the oracle."""
+    from oracle.oracle import oracle_transform
+
+    monkeypatch.setenv("RK_NO_WIDE_PATH", "1")
+    bank = generate_bank(96, 6, 150, GenOptions(seed=4242))
+    values = synth_random(11, 6, 96, seed=4243).values
+    out = transform(values, bank).values
+    assert out.tobytes() == oracle_transform(values, bank).tobytes()
