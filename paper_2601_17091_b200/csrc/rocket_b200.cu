@@ -844,10 +844,10 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   b->cost_prefix.assign(b->chunks.size() + 1, 0);
   for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
 
-  // Wide path: every chunk has <= 2 channel slots.  CTAs per SM as shared
-  // memory allows (at most 6: 6 x 4 warps with up to 4 series per item
-  // measured best at L = 1024), warps per CTA so the SM holds 24 warps (the
-  // ~80-register budget).
+  // Wide path (every bank; fixed slots for 1-2 channels, the run-time slot
+  // loop beyond).  CTAs per SM as shared memory allows (at most 6: 6 x 4
+  // warps with up to 8 series per item measured best at L = 1024), warps per
+  // CTA so the SM holds 24 warps (the ~80-register budget).
   {
     const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
     const int by_smem = (int)((st->smem_optin + 1024) / per_cta);
