@@ -378,7 +378,7 @@ def main():
                                            "scaled to this step's series)" % args.config if traffic else None,
                          "peak_source": "measured FFMA2 microbenchmark (profiles/r01_fp32_peak_microbench.jsonl); "
                                         "MEASURED_PEAKS.json has no FP32 entry",
-                         "kernel": ("rocket_wide_kernel" if info["path"] == 1 else "rocket_class_kernel")
+                         "kernel": ("rocket_class_kernel" if info["path"] == 0 else "rocket_wide_kernel")
                                    + f" x {info['n_launches']} launches (one transform; DESIGN.md §4)"},
             "other_mode": {"mode": other, "ms_per_step": ms_other / args.steps,
                            "value": total_series / (ms_other / 1e3),
@@ -390,7 +390,7 @@ def main():
             "energy": energy,
             "gpu_launches": int(info["n_launches"]) * args.steps,
             "bank": {"groups": info["n_groups"], "chunks": info["n_chunks"], "launches_per_step": info["n_launches"],
-                     "smem_bytes": info["smem_bytes"], "path": ("wide" if info["path"] == 1 else "class"),
+                     "smem_bytes": info["smem_bytes"], "path": {0: "class", 1: "wide", 2: "wide (series in global memory)"}[info["path"]],
                      "ctas_per_sm": info["ctas_per_sm"]},
         }
         print(json.dumps(line), flush=True)

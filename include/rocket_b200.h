@@ -72,8 +72,10 @@ typedef struct rk_bank_info_s {
   int32_t device;
   int32_t n_launches;   /* kernel launches per float32 transform */
   int32_t path;         /* 1: wide kernel (parameter-block weights in
-                           uniform registers); 0: class kernel (banks with
-                           >= 3-channel kernels) */
+                           uniform registers, series staged in shared
+                           memory); 2: wide kernel reading series rows from
+                           global memory (series too long for shared
+                           memory); 0: class kernel (RK_NO_WIDE_PATH) */
   int32_t ctas_per_sm;  /* resident CTAs per SM on the wide path */
 } rk_bank_info_t;
 
@@ -89,8 +91,9 @@ int rk_device_count(int32_t* count);
  * to float32 as in engine._run_range (engine.py:275-276); weight_offsets and
  * channel_offsets are KernelBank.weight_offsets / channel_offsets
  * (kernels.py:84-88).  Replaces the per-batch argument list of the numba
- * call at engine.py:280-295.  Fails with RK_ERR_CAPACITY when one staged
- * series (all channels plus zero halos) does not fit in shared memory. */
+ * call at engine.py:280-295.  A series whose zero-haloed rows do not fit in
+ * one CTA's shared memory is read from global memory instead (slower, no
+ * length limit; rk_bank_info_t.path == 2). */
 int rk_bank_create(int64_t n_kernels, int32_t n_channels, int32_t l_series,
                    const int32_t* lengths, const int32_t* dilations,
                    const int32_t* paddings, const float* biases,

@@ -14,6 +14,8 @@ using WarpFn = void (*)(const WParams);
 // Fill the (class, mode) slots of length LEN: class kernels into cls_tab,
 // wide kernels into wide_tab (index 2 * cls + exact), and the fast-mode MPV
 // wide kernels into mpv_tab (index cls; R capped like exact mode).
-void rk_fill_tables_7(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab);
-void rk_fill_tables_9(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab);
-void rk_fill_tables_11(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab);
+// gmem_tab (index 2 * cls + exact): the variants reading series rows from
+// global memory, for series longer than shared memory holds.
+void rk_fill_tables_7(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);
+void rk_fill_tables_9(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);
+void rk_fill_tables_11(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);

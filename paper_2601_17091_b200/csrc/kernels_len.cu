@@ -28,8 +28,19 @@ void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   }
 }
 
+// GMEM variants: every chunk uses the run-time slot layout; 2-pair chunks
+// at R <= 5, 1-pair chunks at any R (exact mode R <= 7) — within registers.
+template <int RI, int P>
+void fill_gmem(rk::WarpFn* g, int cls) {
+  constexpr int R = rk::r_of(RI);
+  if constexpr (P == 1 || RI <= 2) {
+    g[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 0, false, false, true>;
+    if constexpr (RI <= rk::kExactRIdxCap) g[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 0, true, false, true>;
+  }
+}
+
 template <int RI>
-void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
+void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
   constexpr int R = rk::r_of(RI);
   const int base = (kLenIdx * rk::kNumR + RI) * rk::kNumNck;
   fill_class<RI, 0>(ct, base + 0);
@@ -40,16 +51,20 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
   fill_wide<RI, 1, 2>(dt, mt, base + 1);
   fill_wide<RI, 1, 0>(dt, mt, base + 2);
   fill_wide<RI, 1, 1>(dt, mt, base + 3);
+  fill_gmem<RI, 2>(gt, base + 0);
+  fill_gmem<RI, 1>(gt, base + 1);
+  fill_gmem<RI, 1>(gt, base + 2);
+  fill_gmem<RI, 1>(gt, base + 3);
 }
 }  // namespace
 
 #define RK_CAT2(a, b) a##b
 #define RK_CAT(a, b) RK_CAT2(a, b)
 
-void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt) {
-  fill_r<0>(ct, dt, mt);
-  fill_r<1>(ct, dt, mt);
-  fill_r<2>(ct, dt, mt);
-  fill_r<3>(ct, dt, mt);
-  fill_r<4>(ct, dt, mt);
+void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
+  fill_r<0>(ct, dt, mt, gt);
+  fill_r<1>(ct, dt, mt, gt);
+  fill_r<2>(ct, dt, mt, gt);
+  fill_r<3>(ct, dt, mt, gt);
+  fill_r<4>(ct, dt, mt, gt);
 }

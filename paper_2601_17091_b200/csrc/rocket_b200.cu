@@ -113,6 +113,7 @@ struct rk_bank_s {
     std::vector<rk::float4_t> blob_fast;  // fast mode: weights negated (the series is staged as is)
   };
   bool wide_path = false;  // parameter-block launches, W warps share a series
+  bool gmem = false;       // series too long for shared memory: windows read from zero-haloed rows in global memory
   int wide_ctas_per_sm = 0;  // default CTAs per SM (many series)
   int wide_ctas_smem = 0;    // shared-memory limit of CTAs per SM
   std::vector<WideLaunch> wide_launches;
@@ -207,6 +208,13 @@ struct DeviceState {
   // device-pointer calls: one scratch block per stream (stream order makes
   // reuse safe)
   std::map<cudaStream_t, unsigned long long*> stream_scratch;
+  // GMEM banks: zero-haloed series rows (+ a canonical NaN) per stream
+  struct Rows {
+    float* p = nullptr;
+    size_t floats = 0;
+    int64_t layout = -1;  // (C, L, stride, halo) the halos were zeroed for
+  };
+  std::map<cudaStream_t, Rows> gmem_rows;
 };
 std::mutex g_dev_mu;
 std::map<int, DeviceState*> g_devs;
@@ -244,11 +252,12 @@ using rk::WarpFn;
 struct KernelTable {
   KernelFn fn[2 * rk::kNumClasses] = {};
   WarpFn dfn[2 * rk::kNumClasses] = {};
-  WarpFn mfn[rk::kNumClasses] = {};  // fast-mode MPV wide kernels
+  WarpFn mfn[rk::kNumClasses] = {};      // fast-mode MPV wide kernels
+  WarpFn gfn[2 * rk::kNumClasses] = {};  // series in global memory (GMEM)
   KernelTable() {
-    rk_fill_tables_7(fn, dfn, mfn);
-    rk_fill_tables_9(fn, dfn, mfn);
-    rk_fill_tables_11(fn, dfn, mfn);
+    rk_fill_tables_7(fn, dfn, mfn, gfn);
+    rk_fill_tables_9(fn, dfn, mfn, gfn);
+    rk_fill_tables_11(fn, dfn, mfn, gfn);
   }
 };
 const KernelTable& kernel_table() {
@@ -341,14 +350,15 @@ int exec_cls(int cls, int exact) {
 int c_len(int cls) { return 7 + 2 * (cls / (rk::kNumNck * rk::kNumR)); }
 
 // Wide path: one PDL-chained launch per parameter block, all on `stream`.
-int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
-                int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
+int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out,
+                      int fpk, int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters,
+                      const float* xpad, const float* nanp) {
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   static const bool profile = getenv("RK_PROFILE") != nullptr;
   static rk::WParams params;  // 32 KB: kept off the stack; guarded by the caller's lock
   static std::mutex params_mu;
   std::lock_guard<std::mutex> lk(params_mu);
-  const int smem = b->smem_bytes;
+  const int smem = b->gmem ? 0 : b->smem_bytes;
   // Few series: more, narrower CTAs (down to one warp) so every SM still has
   // work; many series: wide_ctas_per_sm CTAs of 24/ctas warps.
   int ctas = b->wide_ctas_per_sm;
@@ -366,9 +376,17 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
-    // fpk 3 in fast mode: MPV kernels, R capped like exact mode (registers)
-    WarpFn fn = fpk == 3 ? kernel_table().mfn[exec_cls(wl.cls, 1)]
-                         : kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
+    // fpk 3 in fast mode: MPV kernels, R capped like exact mode (registers);
+    // GMEM banks: the global-memory variants (2-pair chunks at R <= 5)
+    WarpFn fn = nullptr;
+    if (b->gmem) {
+      int gc = exec_cls(wl.cls, exact);
+      const int gnck = gc % rk::kNumNck, gri = (gc / rk::kNumNck) % rk::kNumR;
+      if (gnck == 0 && gri > 2) gc += (2 - gri) * rk::kNumNck;
+      fn = kernel_table().gfn[2 * gc + exact];
+    } else {
+      fn = fpk == 3 ? kernel_table().mfn[exec_cls(wl.cls, 1)] : kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
+    }
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (const void*)fn, smem * spi);
     if (rc) return rc;
@@ -393,6 +411,8 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
     h.one = 1.0f;
     h.wbytes = NC * P * len * 8;
     h.spi = spi;
+    h.xpad = xpad;
+    h.nanp = nanp;
     std::memcpy(params.blob, exact ? wl.blob.data() : wl.blob_fast.data(), sizeof(params.blob));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -429,6 +449,51 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
               wl.n_chunks, (long long)grid, ms, wl.dense_flops * (double)n / (ms * 1e-3) / 1e12);
     }
     for (auto e : evs) cudaEventDestroy(e);
+  }
+  return RK_OK;
+}
+
+// Wide path entry: GMEM banks copy each batch of series into zero-haloed
+// rows in a per-stream scratch (halos zeroed once, interiors by a 2-D
+// copy) and run the chain per batch; other banks run the chain directly.
+int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float* d_out, int64_t ld_out, int fpk,
+                int mode, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
+  if (!b->gmem) return launch_wide_chain(b, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters,
+                                         nullptr, nullptr);
+  const int64_t row_floats = (int64_t)b->C * b->sstride;
+  const int64_t budget = ((int64_t)1 << 30) / 4;  // 1 GB of padded rows per batch
+  const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(n, budget / row_floats));
+  const size_t need = (size_t)(batch * row_floats + 4);
+  DeviceState::Rows* rows = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(st->pool_mu);
+    rows = &st->gmem_rows[stream];
+  }
+  // halos (and the NaN) are written when the buffer grows or the row layout
+  // changes; the 2-D copies below only ever write row interiors
+  const int64_t layout = (((int64_t)b->C * 1000003 + b->L) * 1000003 + b->sstride) * 1000003 + b->halo;
+  if (rows->floats < need || rows->layout != layout) {
+    if (rows->floats < need) {
+      if (rows->p) RK_CUDA(cudaFree(rows->p));
+      rows->p = nullptr;
+      RK_CUDA(cudaMalloc(&rows->p, need * sizeof(float)));
+      rows->floats = need;
+    }
+    RK_CUDA(cudaMemsetAsync(rows->p, 0, rows->floats * sizeof(float), stream));
+    const float qnan = __builtin_nanf("");
+    RK_CUDA(cudaMemcpyAsync(rows->p + rows->floats - 1, &qnan, sizeof(float), cudaMemcpyHostToDevice, stream));
+    RK_CUDA(cudaStreamSynchronize(stream));
+    rows->layout = layout;
+  }
+  for (int64_t s0 = 0; s0 < n; s0 += batch) {
+    const int64_t cnt = std::min(batch, n - s0);
+    RK_CUDA(cudaMemcpy2DAsync(rows->p + b->halo, (size_t)b->sstride * sizeof(float), d_x + s0 * b->C * b->L,
+                              (size_t)b->L * sizeof(float), (size_t)b->L * sizeof(float), (size_t)(cnt * b->C),
+                              cudaMemcpyDeviceToDevice, stream));
+    if (s0 > 0) RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
+    const int rc = launch_wide_chain(b, st, d_x, cnt, d_out + s0 * ld_out, ld_out, fpk, mode, stream, d_exec,
+                                     d_counters, rows->p, rows->p + rows->floats - 1);
+    if (rc) return rc;
   }
   return RK_OK;
 }
@@ -515,7 +580,7 @@ int launch(rk_bank_t b, DeviceState* st, const void* d_xv, int64_t n, void* d_ou
   if (n <= 0) return RK_OK;
   // float64, and MPV in exact mode (its ordered positive sum), run the cell
   // kernels; fast-mode MPV runs the wide kernels with summed positives
-  if (esz == 8 || (fpk == 3 && (mode == RK_MODE_EXACT || !b->wide_path)))
+  if (esz == 8 || (fpk == 3 && (mode == RK_MODE_EXACT || !b->wide_path || b->gmem)))
     return launch_cells(b, st, d_xv, esz, n, d_outv, ld_out, fpk, stream, d_exec, d_counters);
   const float* d_x = static_cast<const float*>(d_xv);
   float* d_out = static_cast<float*>(d_outv);
@@ -711,13 +776,18 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   // stride rounded to 32 floats + 1 bank offset between channels.
   const int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + 4;
   const int64_t smem = (int64_t)C * sstride * 4;
-  if (smem > (int64_t)st->smem_optin - 1024)
+  // A series that does not fit in shared memory is read from zero-haloed
+  // rows in global memory instead (L1 / L2 resident; the wide kernel's
+  // GMEM variants, run-time slot layout for every chunk).
+  const bool gmem = smem > (int64_t)st->smem_optin - 1024;
+  if (gmem && getenv("RK_NO_WIDE_PATH"))
     return fail(RK_ERR_CAPACITY,
                 "one staged series needs %lld bytes of shared memory (C=%d, L=%d, halo=%d) but a CTA has %zu",
                 (long long)smem, C, L, halo, st->smem_optin);
 
   std::unique_ptr<rk_bank_s> b(new rk_bank_s());
   b->device = device;
+  b->gmem = gmem;
   b->K = K;
   b->C = C;
   b->L = L;
@@ -779,7 +849,8 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       int64_t best = INT64_MAX;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
         if (nck == 2 && !wide_ok && ri != 0) continue;  // class-kernel generic path: 1 position per lane
-        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), rk::nck_slots(nck) == 0);
+        if (gmem && nck == 0 && ri > 2) continue;  // GMEM slot-loop kernels with 2 pairs: R <= 5 (registers)
+        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), gmem || rk::nck_slots(nck) == 0);
         if (cst < best) {
           best = cst;
           best_r = ri;
@@ -849,8 +920,8 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   // warps with up to 8 series per item measured best at L = 1024), warps per
   // CTA so the SM holds 24 warps (the ~80-register budget).
   {
-    const int per_cta = (int)smem + 1024;  // + the per-CTA reservation
-    const int by_smem = (int)((st->smem_optin + 1024) / per_cta);
+    const int per_cta = (gmem ? 0 : (int)smem) + 1024;  // + the per-CTA reservation
+    const int by_smem = std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / per_cta));
     const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6;
     if (by_smem >= 1 && wide_ok) {
       b->wide_path = true;
@@ -861,7 +932,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         const int cb = b->cls_begin[cls], ce = b->cls_end[cls];
         if (ce <= cb) continue;
         const int nck = cls % rk::kNumNck;
-        const int P = rk::nck_pairs(nck), NC = rk::nck_slots(nck);
+        const int P = rk::nck_pairs(nck), NC = gmem ? 0 : rk::nck_slots(nck);
         const int len = 7 + 2 * (cls / (rk::kNumNck * rk::kNumR));
         // bytes after the descriptor: fixed slots -> the weights; run-time
         // slots -> the weights then the slot list (16-byte aligned)
@@ -1016,7 +1087,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->useful_flops_per_series = b->useful_flops;
   info->device_bytes = b->device_bytes;
   info->device = b->device;
-  info->path = b->wide_path ? 1 : 0;
+  info->path = b->wide_path ? (b->gmem ? 2 : 1) : 0;
   info->ctas_per_sm = b->wide_ctas_per_sm;
   if (b->wide_path)
     info->n_launches = (int32_t)b->wide_launches.size();
@@ -1331,6 +1402,8 @@ int rk_release_caches(void) {
       delete w;
     }
     st->free_workers.clear();
+    for (auto& kv : st->gmem_rows) cudaFree(kv.second.p);
+    st->gmem_rows.clear();
   }
   return RK_OK;
 }

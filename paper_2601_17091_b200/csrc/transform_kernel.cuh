@@ -685,7 +685,11 @@ struct WHeader {
   int vec_in;
   float one;
   int wbytes;  // bytes of weights per chunk
-  int spi;     // series staged per CTA item (wide kernel: 1 or 2)
+  int spi;     // series per CTA item
+  // series too long for shared memory (GMEM kernels): rows of sstride
+  // floats with zero halos in a device scratch, and a canonical NaN there
+  const float* xpad;
+  const float* nanp;
 };
 constexpr int kBlobFloat4 = (kParamBytes - (int)sizeof(WHeader)) / 16;
 struct WParams {
@@ -964,7 +968,7 @@ __device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned 
                : "memory");
 }
 
-template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false>
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
@@ -977,15 +981,20 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
   unsigned phase = 0;
   if (tid == 0) {
     s_nan = __int_as_float(0x7fffffff);
-    if (p.h.vec_in) mbar_init(bar, 1);
+    if (!GMEM && p.h.vec_in) mbar_init(bar, 1);
   }
   const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
   const int SPI = p.h.spi;
   const int slot = C * S;
-  for (int k = tid; k < SPI * slot; k += blockDim.x) {
-    const int t = (k % slot) % S;
-    if (t < H || t >= H + L) smem[k] = 0.0f;
+  if constexpr (!GMEM) {
+    for (int k = tid; k < SPI * slot; k += blockDim.x) {
+      const int t = (k % slot) % S;
+      if (t < H || t >= H + L) smem[k] = 0.0f;
+    }
   }
+  // GMEM: the windows are read from the zero-haloed rows in global memory
+  // (L1 / L2 resident) instead of a staged copy
+  const float* nanp = GMEM ? p.h.nanp : &s_nan;
   const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
   const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
   const float2 one2 = make_float2(p.h.one, p.h.one);
@@ -1004,7 +1013,9 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
     // Stage the item's rows unchanged (FAST negates the weights instead of
     // the series): one bulk copy per row when rows are 16-byte aligned,
     // else a cooperative copy.
-    if (p.h.vec_in) {
+    const float* sbase = GMEM ? p.h.xpad + series0 * slot : smem;
+    if (GMEM) {
+    } else if (p.h.vec_in) {
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
         const unsigned row_bytes = (unsigned)L * 4u;
@@ -1038,8 +1049,8 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         for (int si = 0; si < ns; ++si) {
           Pool<2 * P, MPV> st;
           pool_init<2 * P, EXACT, MPV>(st);
-          run_positions_dyn<LEN, R, P, EXACT, MPV>(st, smem + si * slot + H, slots, nc, wp, S, thr, init, one2,
-                                                   c.lo, c.n, c.d, c.q32, c.r32, c.invd, &s_nan, lane);
+          run_positions_dyn<LEN, R, P, EXACT, MPV>(st, sbase + si * slot + H, slots, nc, wp, S, thr, init, one2,
+                                                   c.lo, c.n, c.d, c.q32, c.r32, c.invd, nanp, lane);
           finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
                                                   p.h.vec_out, lane);
           done += (unsigned long long)c.nk * (unsigned long long)c.n;
@@ -1055,14 +1066,14 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
         // the chunk's weights serve every staged series of the item
         for (int si = 0; si < ns; ++si) {
-          const float* sx = smem + si * slot + H;
+          const float* sx = sbase + si * slot + H;
           const float* chan[NC];
 #pragma unroll
           for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
           Pool<2 * P, MPV> st;
           pool_init<2 * P, EXACT, MPV>(st);
           run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32,
-                                                   c.invd, &s_nan, lane);
+                                                   c.invd, nanp, lane);
           finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
                                                   p.h.vec_out, lane);
           done += (unsigned long long)c.nk * (unsigned long long)c.n;

@@ -190,9 +190,10 @@ def test_errors_mirror_reference(cuda_ready):
         transform(values, bank, limits=GridLimits(max_x=3))
     with pytest.raises(ValueError):
         transform(values, bank, mode="approximate")
+    # a series longer than shared memory holds is no longer a capacity
+    # error: the GMEM kernels read it from global memory (test_gpu_long.py)
     big = generate_bank(200_000, 1, 4, GenOptions(seed=3))
-    with pytest.raises(CapacityError):
-        transform(np.zeros((1, 1, 200_000), dtype=np.float32), big)
+    assert transform(np.zeros((1, 1, 200_000), dtype=np.float32), big).values.shape == (1, 8)
 
 
 OTHER = [(name, v) for name, case in gc.CASES.items() for v in case["variants"] if v != "single"]
