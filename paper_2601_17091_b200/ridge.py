@@ -73,6 +73,27 @@ def _chol_solve(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     return torch.cholesky_solve(B, L)
 
 
+def _gram_rows(X: torch.Tensor, blocks: int = 4) -> torch.Tensor:
+    """X X^T using its symmetry: the upper block triangle of a `blocks` x
+    `blocks` split (10 of 16 GEMM blocks for 4), mirrored.  The n x n Gram of
+    the dual solve is the FP64-GEMM-bound step of a ridge fit."""
+    n = X.shape[0]
+    if n < 512 or X.device.type != "cuda":
+        return X @ X.T
+    edges = [n * i // blocks for i in range(blocks + 1)]
+    G = torch.empty((n, n), dtype=X.dtype, device=X.device)
+    for i in range(blocks):
+        a0, a1 = edges[i], edges[i + 1]
+        Xa = X[a0:a1]
+        for j in range(i, blocks):
+            b0, b1 = edges[j], edges[j + 1]
+            blk = Xa @ X[b0:b1].T
+            G[a0:a1, b0:b1] = blk
+            if j != i:
+                G[b0:b1, a0:a1] = blk.T
+    return G
+
+
 def solve_penalized(X, Y, alpha: float):
     """Solve (X'X + alpha I) W = X'Y in float64 (ridge.py:100-122)."""
     if alpha <= 0:
@@ -84,11 +105,11 @@ def solve_penalized(X, Y, alpha: float):
         Y = Y[:, None]
     n, f = X.shape
     if f <= n:
-        gram = X.T @ X
+        gram = _gram_rows(X.T)
         gram.diagonal().add_(alpha)
         W = _chol_solve(gram, X.T @ Y)
     else:
-        outer = X @ X.T
+        outer = _gram_rows(X)
         outer.diagonal().add_(alpha)
         W = X.T @ _chol_solve(outer, Y)
     return W[:, 0] if single else W
