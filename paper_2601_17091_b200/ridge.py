@@ -276,7 +276,7 @@ def fit_sharded(local_features, local_labels, alpha: float = 1.0, group=None, de
     Xs = (X - means) / scales
     f = X.shape[1]
     if f <= n:
-        gram = Xs.T @ Xs
+        gram = _gram_rows(Xs.T)
         rhs = Xs.T @ Y
         dist.all_reduce(gram, group=group)
         dist.all_reduce(rhs, group=group)
