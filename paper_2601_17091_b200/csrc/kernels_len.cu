@@ -29,7 +29,7 @@ void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
 }
 
 // GMEM variants: every chunk uses the run-time slot layout; 2-pair chunks
-// at R <= 5, 1-pair chunks at any R (exact mode R <= 7) — within registers.
+// at R <= 5, 1-pair chunks at any R — within registers.
 template <int RI, int P>
 void fill_gmem(rk::WarpFn* g, int cls) {
   constexpr int R = rk::r_of(RI);

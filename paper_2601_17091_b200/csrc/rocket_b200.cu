@@ -338,7 +338,7 @@ bool is_pinned_host(const void* p) {
 }
 
 // The class a launch executes: exact mode runs the largest-R class with the
-// R = 7 instantiation (same chunks, only positions per lane differ).
+// R capped at r_of(kExactRIdxCap) (same chunks, only positions per lane differ).
 int exec_cls(int cls, int exact) {
   const int nck = cls % rk::kNumNck;
   const int ri = (cls / rk::kNumNck) % rk::kNumR;
@@ -376,7 +376,7 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
-    // fpk 3 in fast mode: MPV kernels, R capped like exact mode (registers);
+    // fpk 3 in fast mode: MPV kernels (R capped like exact mode);
     // GMEM banks: the global-memory variants (2-pair chunks at R <= 5)
     WarpFn fn = nullptr;
     if (b->gmem) {

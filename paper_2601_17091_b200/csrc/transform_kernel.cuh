@@ -68,7 +68,10 @@ constexpr int kNumR = 5;
 // over the shared-memory banks).  Exact-mode launches run the RK_RMAX class
 // with the R = 7 kernel (its FMUL2 temporaries leave no room for 11).
 __host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 4 ? RK_RMAX : 2 * r_idx + 1; }
-constexpr int kExactRIdxCap = 3;
+#ifndef RK_EXACT_RIDX_CAP
+#define RK_EXACT_RIDX_CAP 4  // exact (and fast-MPV) launches may use every R (was 3: R <= 7)
+#endif
+constexpr int kExactRIdxCap = RK_EXACT_RIDX_CAP;
 constexpr int kNumNck = 4;
 // (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop
 __host__ __device__ constexpr int nck_pairs(int nck) { return nck == 0 ? 2 : 1; }
