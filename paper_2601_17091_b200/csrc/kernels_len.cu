@@ -67,4 +67,5 @@ void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpF
   fill_r<2>(ct, dt, mt, gt);
   fill_r<3>(ct, dt, mt, gt);
   fill_r<4>(ct, dt, mt, gt);
+  if constexpr (rk::kNumR > 5) fill_r<5>(ct, dt, mt, gt);
 }

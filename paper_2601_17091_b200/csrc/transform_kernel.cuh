@@ -63,13 +63,17 @@ constexpr unsigned kFull = 0xffffffffu;
 //           2: >= 3 channels, 1 pair (wide kernel: channel slots looped at
 //              run time; class kernel: the generic 1-position path);
 //           3: 1 channel, 1 pair
-constexpr int kNumR = 5;
-// positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX (odd: spreads lanes
-// over the shared-memory banks).  Exact-mode launches run the RK_RMAX class
-// with the R = 7 kernel (its FMUL2 temporaries leave no room for 11).
-__host__ __device__ constexpr int r_of(int r_idx) { return r_idx == 4 ? RK_RMAX : 2 * r_idx + 1; }
+#ifndef RK_NUM_R
+#define RK_NUM_R 6
+#endif
+constexpr int kNumR = RK_NUM_R;  // R = 1, 3, 5, 7, RK_RMAX (11), 13
+// positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX, 13 (odd: spreads
+// lanes over the shared-memory banks); the cost model picks one per chunk.
+__host__ __device__ constexpr int r_of(int r_idx) {
+  return r_idx == 5 ? 13 : r_idx == 4 ? RK_RMAX : 2 * r_idx + 1;
+}
 #ifndef RK_EXACT_RIDX_CAP
-#define RK_EXACT_RIDX_CAP 4  // exact (and fast-MPV) launches may use every R (was 3: R <= 7)
+#define RK_EXACT_RIDX_CAP 5  // exact (and fast-MPV) launches may use every R (was 3: R <= 7)
 #endif
 constexpr int kExactRIdxCap = RK_EXACT_RIDX_CAP;
 constexpr int kNumNck = 4;
