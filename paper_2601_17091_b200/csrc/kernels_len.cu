@@ -9,20 +9,20 @@
 namespace {
 constexpr int kLenIdx = (RK_LEN - 7) / 2;
 
-// Exact mode never runs R above r_of(kExactRIdxCap) (exec_cls caps it), so
-// those exact variants are not instantiated.
+// Exact mode never runs R above kExactRMax (exec_cls caps it), so those
+// exact variants are not instantiated.
 template <int RI, int NCK>
 void fill_class(rk::KernelFn* t, int cls) {
   constexpr int R = rk::r_of(RI);
   t[2 * cls + 0] = rk::rocket_class_kernel<RK_LEN, R, NCK, false>;
-  if constexpr (RI <= rk::kExactRIdxCap) t[2 * cls + 1] = rk::rocket_class_kernel<RK_LEN, R, NCK, true>;
+  if constexpr (R <= rk::kExactRMax) t[2 * cls + 1] = rk::rocket_class_kernel<RK_LEN, R, NCK, true>;
 }
 
 template <int RI, int P, int NC>
 void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   constexpr int R = rk::r_of(RI);
   wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false>;
-  if constexpr (RI <= rk::kExactRIdxCap) {
+  if constexpr (R <= rk::kExactRMax) {
     wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, true>;
     mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, NC, false, true>;
   }
@@ -35,7 +35,7 @@ void fill_gmem(rk::WarpFn* g, int cls) {
   constexpr int R = rk::r_of(RI);
   if constexpr (P == 1 || RI <= 2) {
     g[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 0, false, false, true>;
-    if constexpr (RI <= rk::kExactRIdxCap) g[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 0, true, false, true>;
+    if constexpr (R <= rk::kExactRMax) g[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 0, true, false, true>;
   }
 }
 
@@ -68,4 +68,6 @@ void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpF
   fill_r<3>(ct, dt, mt, gt);
   fill_r<4>(ct, dt, mt, gt);
   if constexpr (rk::kNumR > 5) fill_r<5>(ct, dt, mt, gt);
+  if constexpr (rk::kNumR > 6) fill_r<6>(ct, dt, mt, gt);
+  if constexpr (rk::kNumR > 7) fill_r<7>(ct, dt, mt, gt);
 }

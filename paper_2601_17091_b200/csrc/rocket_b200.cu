@@ -337,13 +337,13 @@ bool is_pinned_host(const void* p) {
   return attr.type == cudaMemoryTypeHost;
 }
 
-// The class a launch executes: exact mode runs the largest-R class with the
-// R capped at r_of(kExactRIdxCap) (same chunks, only positions per lane differ).
+// The class a launch executes: exact mode (and fast MPV) run classes above
+// R = kExactRMax with that R (same chunks, only positions per lane differ).
 int exec_cls(int cls, int exact) {
   const int nck = cls % rk::kNumNck;
   const int ri = (cls / rk::kNumNck) % rk::kNumR;
   const int li = cls / (rk::kNumNck * rk::kNumR);
-  const int r = exact ? std::min(ri, rk::kExactRIdxCap) : ri;
+  const int r = exact && rk::r_of(ri) > rk::kExactRMax ? rk::kExactRIdx13 : ri;
   return (li * rk::kNumR + r) * rk::kNumNck + nck;
 }
 

@@ -64,18 +64,20 @@ constexpr unsigned kFull = 0xffffffffu;
 //              run time; class kernel: the generic 1-position path);
 //           3: 1 channel, 1 pair
 #ifndef RK_NUM_R
-#define RK_NUM_R 6
+#define RK_NUM_R 8
 #endif
-constexpr int kNumR = RK_NUM_R;  // R = 1, 3, 5, 7, RK_RMAX (11), 13
-// positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX, 13 (odd: spreads
-// lanes over the shared-memory banks); the cost model picks one per chunk.
+constexpr int kNumR = RK_NUM_R;  // R = 1, 3, 5, 7, RK_RMAX (11), 13, 9, 15
+// positions per lane of class r_idx: 1, 3, 5, 7, RK_RMAX, 13, 9, 15 (odd:
+// spreads lanes over the shared-memory banks); the cost model picks one per
+// chunk.
 __host__ __device__ constexpr int r_of(int r_idx) {
-  return r_idx == 5 ? 13 : r_idx == 4 ? RK_RMAX : 2 * r_idx + 1;
+  return r_idx == 7 ? 15 : r_idx == 6 ? 9 : r_idx == 5 ? 13 : r_idx == 4 ? RK_RMAX : 2 * r_idx + 1;
 }
-#ifndef RK_EXACT_RIDX_CAP
-#define RK_EXACT_RIDX_CAP 5  // exact (and fast-MPV) launches may use every R (was 3: R <= 7)
-#endif
-constexpr int kExactRIdxCap = RK_EXACT_RIDX_CAP;
+// exact mode and fast-mode MPV: R <= 13 (their FMUL2 temporaries / partial
+// sums spill at 15); a larger class runs at the R = 13 index
+constexpr int kExactRMax = 13;
+constexpr int kExactRIdx13 = 5;
+static_assert(r_of(kExactRIdx13) == kExactRMax, "R class table");
 constexpr int kNumNck = 4;
 // (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop
 __host__ __device__ constexpr int nck_pairs(int nck) { return nck == 0 ? 2 : 1; }
