@@ -453,6 +453,9 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   return RK_OK;
 }
 
+int padded_rows(rk_bank_t b, DeviceState* st, cudaStream_t stream, int esz, const void* d_x, int64_t rows,
+                void** out);
+
 // Wide path entry: GMEM banks copy each batch of series into zero-haloed
 // rows in a per-stream scratch (halos zeroed once, interiors by a 2-D
 // copy) and run the chain per batch; other banks run the chain directly.
@@ -463,52 +466,37 @@ int launch_wide(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n, float
   const int64_t row_floats = (int64_t)b->C * b->sstride;
   const int64_t budget = ((int64_t)1 << 30) / 4;  // 1 GB of padded rows per batch
   const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(n, budget / row_floats));
-  const size_t need = (size_t)(batch * row_floats + 4);
-  DeviceState::Rows* rows = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(st->pool_mu);
-    rows = &st->gmem_rows[stream];
-  }
-  // halos (and the NaN) are written when the buffer grows or the row layout
-  // changes; the 2-D copies below only ever write row interiors
-  const int64_t layout = (((int64_t)b->C * 1000003 + b->L) * 1000003 + b->sstride) * 1000003 + b->halo;
-  if (rows->floats < need || rows->layout != layout) {
-    if (rows->floats < need) {
-      if (rows->p) RK_CUDA(cudaFree(rows->p));
-      rows->p = nullptr;
-      RK_CUDA(cudaMalloc(&rows->p, need * sizeof(float)));
-      rows->floats = need;
-    }
-    RK_CUDA(cudaMemsetAsync(rows->p, 0, rows->floats * sizeof(float), stream));
-    const float qnan = __builtin_nanf("");
-    RK_CUDA(cudaMemcpyAsync(rows->p + rows->floats - 1, &qnan, sizeof(float), cudaMemcpyHostToDevice, stream));
-    RK_CUDA(cudaStreamSynchronize(stream));
-    rows->layout = layout;
-  }
   for (int64_t s0 = 0; s0 < n; s0 += batch) {
     const int64_t cnt = std::min(batch, n - s0);
-    RK_CUDA(cudaMemcpy2DAsync(rows->p + b->halo, (size_t)b->sstride * sizeof(float), d_x + s0 * b->C * b->L,
-                              (size_t)b->L * sizeof(float), (size_t)b->L * sizeof(float), (size_t)(cnt * b->C),
-                              cudaMemcpyDeviceToDevice, stream));
+    void* rows = nullptr;
+    int rc = padded_rows(b, st, stream, 4, d_x + s0 * b->C * b->L, cnt, &rows);
+    if (rc) return rc;
+    const float* xpad = static_cast<const float*>(rows);
+    const float* nanp = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(st->pool_mu);
+      const auto& r = st->gmem_rows[stream];
+      nanp = r.p + r.floats - 1;
+    }
     if (s0 > 0) RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * kMaxLaunches, stream));
-    const int rc = launch_wide_chain(b, st, d_x, cnt, d_out + s0 * ld_out, ld_out, fpk, mode, stream, d_exec,
-                                     d_counters, rows->p, rows->p + rows->floats - 1);
+    rc = launch_wide_chain(b, st, d_x, cnt, d_out + s0 * ld_out, ld_out, fpk, mode, stream, d_exec, d_counters,
+                           xpad, nanp);
     if (rc) return rc;
   }
   return RK_OK;
 }
 
-// Cell path: precision "double" (esz 8) or MPV (fpk 3).
-// float64 (precision "double") and MPV (fpk = 3): the reference loop order
-// on the CUDA cores.  The staged cell kernel (one series in shared memory,
-// one launch per kernel length) when a series fits; otherwise the unstaged
-// cell kernel reading the series from global memory.
+// Cell path: float64 (precision "double") and exact MPV (fpk = 3): the
+// reference loop order on the CUDA cores.  The staged cell kernel (one
+// series in shared memory, one launch per kernel length) when a series fits;
+// otherwise the same kernel reading zero-haloed rows from global memory
+// (RK_NO_CELLROW: the unstaged thread-per-cell kernel).
 #ifndef RK_CELL_B
 #define RK_CELL_B 4  // positions per block (independent accumulation chains)
 #endif
-template <typename T, bool MPV, int LEN>
+template <typename T, bool MPV, int LEN, bool GMEM>
 int launch_cellrow(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStream_t stream) {
-  auto fn = rk::rocket_cellrow_kernel<T, MPV, LEN, RK_CELL_B>;
+  auto fn = rk::rocket_cellrow_kernel<T, MPV, LEN, RK_CELL_B, GMEM>;
   int rc = set_kernel_smem(st, (const void*)fn, (int)smem);
   if (rc) return rc;
   int per_sm = 1;
@@ -519,9 +507,9 @@ int launch_cellrow(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStre
   return RK_OK;
 }
 
-template <typename T, bool MPV>
+template <typename T, bool MPV, bool GMEM>
 int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t stream, int* d_counters) {
-  const size_t smem = (size_t)b->C * b->sstride * sizeof(T);
+  const size_t smem = GMEM ? 0 : (size_t)b->C * b->sstride * sizeof(T);
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * 3, stream));
   a.halo = b->halo;
   a.sstride = b->sstride;
@@ -530,9 +518,65 @@ int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t s
     a.k_begin = (int)b->cell_len_begin[li];
     a.k_end = (int)b->cell_len_end[li];
     a.item_counter = d_counters + li;
-    const int rc = li == 0 ? launch_cellrow<T, MPV, 7>(st, a, smem, stream)
-                 : li == 1 ? launch_cellrow<T, MPV, 9>(st, a, smem, stream)
-                           : launch_cellrow<T, MPV, 11>(st, a, smem, stream);
+    const int rc = li == 0 ? launch_cellrow<T, MPV, 7, GMEM>(st, a, smem, stream)
+                 : li == 1 ? launch_cellrow<T, MPV, 9, GMEM>(st, a, smem, stream)
+                           : launch_cellrow<T, MPV, 11, GMEM>(st, a, smem, stream);
+    if (rc) return rc;
+  }
+  return RK_OK;
+}
+
+// Zero-haloed rows of `esz`-byte elements for `rows` series in a per-stream
+// scratch: halos zeroed when the buffer grows or the layout changes, row
+// interiors by one 2-D copy per call.
+int padded_rows(rk_bank_t b, DeviceState* st, cudaStream_t stream, int esz, const void* d_x, int64_t rows,
+                void** out) {
+  const int64_t row_elems = (int64_t)b->C * b->sstride;
+  const size_t need = (size_t)(rows * row_elems + 4) * esz;
+  DeviceState::Rows* r = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(st->pool_mu);
+    r = &st->gmem_rows[stream];
+  }
+  const int64_t layout = ((((int64_t)b->C * 1000003 + b->L) * 1000003 + b->sstride) * 1000003 + b->halo) * 16 + esz;
+  if (r->floats * sizeof(float) < need || r->layout != layout) {
+    if (r->floats * sizeof(float) < need) {
+      if (r->p) RK_CUDA(cudaFree(r->p));
+      r->p = nullptr;
+      RK_CUDA(cudaMalloc(&r->p, need));
+      r->floats = need / sizeof(float);
+    }
+    RK_CUDA(cudaMemsetAsync(r->p, 0, r->floats * sizeof(float), stream));
+    const float qnan = __builtin_nanf("");
+    RK_CUDA(cudaMemcpyAsync(r->p + r->floats - 1, &qnan, sizeof(float), cudaMemcpyHostToDevice, stream));
+    RK_CUDA(cudaStreamSynchronize(stream));
+    r->layout = layout;
+  }
+  RK_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(r->p) + (size_t)b->halo * esz, (size_t)b->sstride * esz, d_x,
+                            (size_t)b->L * esz, (size_t)b->L * esz, (size_t)(rows * b->C), cudaMemcpyDeviceToDevice,
+                            stream));
+  *out = r->p;
+  return RK_OK;
+}
+
+// Cell kernels over series too long for shared memory: batches of padded
+// rows in global memory (1 GB of rows per batch).
+template <typename T, bool MPV>
+int launch_cellrows_gmem(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t stream, int* d_counters) {
+  const int64_t row_elems = (int64_t)b->C * b->sstride;
+  const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(a.n_series, (((int64_t)1 << 30) / sizeof(T)) /
+                                                                            row_elems));
+  const int64_t n = a.n_series;
+  for (int64_t s0 = 0; s0 < n; s0 += batch) {
+    const int64_t cnt = std::min(batch, n - s0);
+    void* rows = nullptr;
+    int rc = padded_rows(b, st, stream, (int)sizeof(T), static_cast<const T*>(a.x) + s0 * b->C * b->L, cnt, &rows);
+    if (rc) return rc;
+    rk::CellArgs ab = a;
+    ab.n_series = cnt;
+    ab.xpad = rows;
+    ab.out = static_cast<T*>(a.out) + s0 * a.ld_out;
+    rc = launch_cellrows<T, MPV, true>(b, st, ab, stream, d_counters);
     if (rc) return rc;
   }
   return RK_OK;
@@ -556,11 +600,17 @@ int launch_cells(rk_bank_t b, DeviceState* st, const void* d_x, int esz, int64_t
   a.n_channels = b->C;
   a.fpk = fpk;
   const size_t staged = (size_t)b->C * b->sstride * esz;
-  if (staged + 1024 <= st->smem_optin && !getenv("RK_NO_CELLROW")) {
+  if (!getenv("RK_NO_CELLROW")) {
+    if (staged + 1024 <= st->smem_optin) {
+      if (esz == 8)
+        return fpk == 3 ? launch_cellrows<double, true, false>(b, st, a, stream, d_counters)
+                        : launch_cellrows<double, false, false>(b, st, a, stream, d_counters);
+      return launch_cellrows<float, true, false>(b, st, a, stream, d_counters);
+    }
     if (esz == 8)
-      return fpk == 3 ? launch_cellrows<double, true>(b, st, a, stream, d_counters)
-                      : launch_cellrows<double, false>(b, st, a, stream, d_counters);
-    return launch_cellrows<float, true>(b, st, a, stream, d_counters);
+      return fpk == 3 ? launch_cellrows_gmem<double, true>(b, st, a, stream, d_counters)
+                      : launch_cellrows_gmem<double, false>(b, st, a, stream, d_counters);
+    return launch_cellrows_gmem<float, true>(b, st, a, stream, d_counters);
   }
   dim3 grid((unsigned)((b->K + 127) / 128), (unsigned)std::min<int64_t>(n, 65535));
   if (esz == 8) {

@@ -744,6 +744,7 @@ struct CellArgs {
   int k_begin, k_end;    // sorted-kernel range of this launch (one length)
   int halo;              // zero halo per side of a staged row (elements)
   int sstride;           // elements per staged channel row
+  const void* xpad;      // GMEM: zero-haloed rows of this launch's series
 };
 
 template <typename T>
@@ -821,16 +822,18 @@ __global__ void __launch_bounds__(128) rocket_cell_kernel(const CellArgs a) {
 // are sorted by (length, channels, dilation, padding) so the lanes of a
 // warp mostly read the same smem word (a broadcast) and run equal trip
 // counts.
-template <typename T, bool MPV, int LEN, int B>
+template <typename T, bool MPV, int LEN, int B, bool GMEM = false>
 __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
   extern __shared__ __align__(16) unsigned char cell_smem[];
-  T* xs = reinterpret_cast<T*>(cell_smem);
+  T* xstage = reinterpret_cast<T*>(cell_smem);
   __shared__ int s_item, s_next;
   const int tid = threadIdx.x, lane = tid & 31;
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
-  for (int k = tid; k < C * S; k += blockDim.x) {
-    const int t = k % S;
-    if (t < H || t >= H + L) xs[k] = T(0);
+  if constexpr (!GMEM) {
+    for (int k = tid; k < C * S; k += blockDim.x) {
+      const int t = k % S;
+      if (t < H || t >= H + L) xstage[k] = T(0);
+    }
   }
   const int ngroups = (a.k_end - a.k_begin + 31) / 32;
   const T* wts = reinterpret_cast<const T*>(a.weights);
@@ -845,12 +848,17 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
     __syncthreads();
     const int64_t i = s_item;
     if (i >= a.n_series) break;
-    const T* xi = reinterpret_cast<const T*>(a.x) + i * (int64_t)C * L;
-    for (int k = tid; k < C * L; k += blockDim.x) {
-      const int c = k / L, t = k - c * L;
-      xs[c * S + H + t] = xi[k];
+    // GMEM: the series' zero-haloed rows are read from global memory (a
+    // series too long for shared memory); otherwise staged here
+    const T* xs = GMEM ? reinterpret_cast<const T*>(a.xpad) + i * (int64_t)C * S : xstage;
+    if constexpr (!GMEM) {
+      const T* xi = reinterpret_cast<const T*>(a.x) + i * (int64_t)C * L;
+      for (int k = tid; k < C * L; k += blockDim.x) {
+        const int c = k / L, t = k - c * L;
+        xstage[c * S + H + t] = xi[k];
+      }
+      __syncthreads();
     }
-    __syncthreads();
     while (true) {
       int g = 0;
       if (lane == 0) g = atomicAdd(&s_next, 1);
