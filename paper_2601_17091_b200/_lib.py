@@ -86,14 +86,23 @@ def build(verbose=False, out=None, defines=()):
              ("rocket_stream.o", os.path.join(CSRC, "rocket_stream.cu"), []),
              # host-only; no FMA contraction so the doubles round like numpy's
              ("bank_gen.o", os.path.join(CSRC, "bank_gen.cpp"), ["-Xcompiler", "-ffp-contract=off"])]
-    units += [(f"kernels_len{n}.o", os.path.join(CSRC, "kernels_len.cu"), [f"-DRK_LEN={n}"]) for n in (7, 9, 11)]
-    procs = []
+    # one unit per (tap length, R class): 24 template-heavy units in parallel
+    units += [(f"kernels_len{n}_r{ri}.o", os.path.join(CSRC, "kernels_len.cu"), [f"-DRK_LEN={n}", f"-DRK_RI={ri}"])
+              for n in (7, 9, 11) for ri in range(8)]
+    jobs = max(1, os.cpu_count() or 1)
+    running, failed = [], []
     for obj, src, extra in units:
         cmd = ["nvcc", *flags, *extra, "-c", "-o", os.path.join(objdir, obj), src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        procs.append((cmd, subprocess.Popen(cmd)))
-    failed = [cmd for cmd, p in procs if p.wait() != 0]
+        while len(running) >= jobs:
+            c, p = running.pop(0)
+            if p.wait() != 0:
+                failed.append(c)
+        running.append((cmd, subprocess.Popen(cmd)))
+    for c, p in running:
+        if p.wait() != 0:
+            failed.append(c)
     if failed:
         raise subprocess.CalledProcessError(1, failed[0])
     link = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out,

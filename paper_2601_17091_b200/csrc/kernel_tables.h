@@ -11,11 +11,17 @@ using KernelFn = void (*)(const LaunchArgs);
 using WarpFn = void (*)(const WParams);
 }  // namespace rk
 
-// Fill the (class, mode) slots of length LEN: class kernels into cls_tab,
-// wide kernels into wide_tab (index 2 * cls + exact), and the fast-mode MPV
-// wide kernels into mpv_tab (index cls; R capped like exact mode).
-// gmem_tab (index 2 * cls + exact): the variants reading series rows from
-// global memory, for series longer than shared memory holds.
-void rk_fill_tables_7(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);
-void rk_fill_tables_9(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);
-void rk_fill_tables_11(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, rk::WarpFn* gmem_tab);
+// Fill the (class, mode) slots of length LEN and R class RI: class kernels
+// into cls_tab, wide kernels into wide_tab (index 2 * cls + exact), the
+// fast-mode MPV wide kernels into mpv_tab (index cls), and the variants
+// reading series rows from global memory (series longer than shared memory
+// holds) into gmem_tab (index 2 * cls + exact).
+#define RK_FILL_DECL(L, R)                                                                               \
+  void rk_fill_tables_##L##_##R(rk::KernelFn* cls_tab, rk::WarpFn* wide_tab, rk::WarpFn* mpv_tab, \
+                                rk::WarpFn* gmem_tab);
+#define RK_FILL_DECL_L(L) \
+  RK_FILL_DECL(L, 0) RK_FILL_DECL(L, 1) RK_FILL_DECL(L, 2) RK_FILL_DECL(L, 3) RK_FILL_DECL(L, 4) \
+  RK_FILL_DECL(L, 5) RK_FILL_DECL(L, 6) RK_FILL_DECL(L, 7)
+RK_FILL_DECL_L(7)
+RK_FILL_DECL_L(9)
+RK_FILL_DECL_L(11)

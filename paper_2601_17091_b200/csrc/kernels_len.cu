@@ -1,9 +1,10 @@
-// kernels_len.cu — instantiates every kernel of one tap length (RK_LEN)
-// and exports the table filler declared in kernel_tables.h.
+// kernels_len.cu — instantiates the kernels of one tap length (RK_LEN) and
+// one positions-per-lane class (RK_RI) and exports the table filler declared
+// in kernel_tables.h; the 3 x 8 units build in parallel.
 #include "kernel_tables.h"
 
-#ifndef RK_LEN
-#error "compile with -DRK_LEN=7|9|11"
+#if !defined(RK_LEN) || !defined(RK_RI)
+#error "compile with -DRK_LEN=7|9|11 -DRK_RI=0..7"
 #endif
 
 namespace {
@@ -58,16 +59,9 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
 }
 }  // namespace
 
-#define RK_CAT2(a, b) a##b
-#define RK_CAT(a, b) RK_CAT2(a, b)
+#define RK_CAT2(a, b, c) a##b##_##c
+#define RK_CAT(a, b, c) RK_CAT2(a, b, c)
 
-void RK_CAT(rk_fill_tables_, RK_LEN)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
-  fill_r<0>(ct, dt, mt, gt);
-  fill_r<1>(ct, dt, mt, gt);
-  fill_r<2>(ct, dt, mt, gt);
-  fill_r<3>(ct, dt, mt, gt);
-  fill_r<4>(ct, dt, mt, gt);
-  if constexpr (rk::kNumR > 5) fill_r<5>(ct, dt, mt, gt);
-  if constexpr (rk::kNumR > 6) fill_r<6>(ct, dt, mt, gt);
-  if constexpr (rk::kNumR > 7) fill_r<7>(ct, dt, mt, gt);
+void RK_CAT(rk_fill_tables_, RK_LEN, RK_RI)(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
+  if constexpr (RK_RI < rk::kNumR) fill_r<RK_RI>(ct, dt, mt, gt);
 }

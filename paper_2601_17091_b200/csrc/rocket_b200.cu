@@ -255,9 +255,14 @@ struct KernelTable {
   WarpFn mfn[rk::kNumClasses] = {};      // fast-mode MPV wide kernels
   WarpFn gfn[2 * rk::kNumClasses] = {};  // series in global memory (GMEM)
   KernelTable() {
-    rk_fill_tables_7(fn, dfn, mfn, gfn);
-    rk_fill_tables_9(fn, dfn, mfn, gfn);
-    rk_fill_tables_11(fn, dfn, mfn, gfn);
+#define RK_FILL(L, R) rk_fill_tables_##L##_##R(fn, dfn, mfn, gfn);
+#define RK_FILL_L(L) RK_FILL(L, 0) RK_FILL(L, 1) RK_FILL(L, 2) RK_FILL(L, 3) RK_FILL(L, 4) RK_FILL(L, 5) \
+    RK_FILL(L, 6) RK_FILL(L, 7)
+    RK_FILL_L(7)
+    RK_FILL_L(9)
+    RK_FILL_L(11)
+#undef RK_FILL_L
+#undef RK_FILL
   }
 };
 const KernelTable& kernel_table() {
