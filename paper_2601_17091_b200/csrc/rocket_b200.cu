@@ -208,6 +208,10 @@ struct DeviceState {
   // device-pointer calls: one scratch block per stream (stream order makes
   // reuse safe)
   std::map<cudaStream_t, unsigned long long*> stream_scratch;
+  // one transform's counter reset, launch chain and counter read at a time
+  // per stream: concurrent callers on one stream (e.g. the library's default
+  // stream) must not interleave them
+  std::map<cudaStream_t, std::unique_ptr<std::mutex>> stream_mu;
   // GMEM banks: zero-haloed series rows (+ a canonical NaN) per stream
   struct Rows {
     float* p = nullptr;
@@ -1175,6 +1179,14 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
     // Device-resident: asynchronous on the caller's stream (or the
     // library's); the counters live in that stream's scratch block.
     cudaStream_t stream = stream_ptr ? (cudaStream_t)stream_ptr : st->stream;
+    std::mutex* smu = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(st->pool_mu);
+      auto& m = st->stream_mu[stream];
+      if (!m) m.reset(new std::mutex());
+      smu = m.get();
+    }
+    std::lock_guard<std::mutex> stream_lock(*smu);
     unsigned long long* d_exec = nullptr;
     rc = stream_scratch(st, stream, &d_exec);
     if (rc) return rc;

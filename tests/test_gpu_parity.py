@@ -300,3 +300,40 @@ def test_class_kernel_path_still_exact(cuda_ready, monkeypatch):
     values = synth_random(11, 6, 96, seed=4243).values
     out = transform(values, bank).values
     assert out.tobytes() == oracle_transform(values, bank).tobytes()
+
+
+def test_concurrent_callers_on_one_stream(cuda_ready):
+    """Several host threads transforming device buffers on the library's
+    default stream (stream=None) at once: each call's counter reset, launch
+    chain and executed-count read stay together (SPEC.md:267 — safe from
+    concurrent callers on distinct outputs)."""
+    import threading
+
+    import torch
+
+    bank = generate_bank(256, 1, 600, GenOptions(seed=31))
+    db = device_bank(bank, 0)
+    xs = [torch.from_numpy(synth_random(300 + 17 * i, 1, 256, seed=40 + i).values).cuda() for i in range(6)]
+    ref = [transform(x.cpu().numpy(), bank).values for x in xs]
+    outs = [torch.empty((x.shape[0], bank.count * 2), device="cuda") for x in xs]
+    executed = [0] * len(xs)
+    errors = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                executed[i] = db.transform_into(xs[i].data_ptr(), xs[i].shape[0], outs[i].data_ptr(),
+                                                bank.count * 2, mode="exact")
+        except BaseException as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(xs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors
+    torch.cuda.synchronize()
+    for i, x in enumerate(xs):
+        assert outs[i].cpu().numpy().tobytes() == ref[i].tobytes()
+        assert executed[i] == expected_dot_products(bank, x.shape[0])
