@@ -316,6 +316,8 @@ int run_stream(rk_bank_t bank, const StreamIO& io, int64_t n, int32_t dtype, int
     static const int64_t mb = getenv("RK_STREAM_BATCH_MB") ? std::max(1, atoi(getenv("RK_STREAM_BATCH_MB"))) : 256;
     batch = std::max<int64_t>(4096, (mb << 20) / std::max<int64_t>(1, out_row));
     batch = std::min<int64_t>(batch, 65535);
+    // long series: bound the pinned input slots too
+    batch = std::min<int64_t>(batch, std::max<int64_t>(64, ((int64_t)512 << 20) / std::max<int64_t>(1, dev_row)));
   }
   batch = std::min(batch, n);
   const int64_t nb = (n + batch - 1) / batch;
