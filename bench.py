@@ -142,7 +142,7 @@ def cpu_sample_rate(bank, cfg, seconds, seed=1):
     from paper_2601_17091_b200 import synth_random
 
     threads = os.cpu_count() or 1
-    probe = max(1, threads // 2)
+    probe = threads  # one series per thread, so the probe rate is the full-machine rate
     x = synth_random(probe, cfg["c"], cfg["l"], seed=seed).values
     t0 = time.perf_counter()
     oracle_transform(x, bank, nthreads=threads)
