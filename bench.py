@@ -144,6 +144,7 @@ def cpu_sample_rate(bank, cfg, seconds, seed=1):
     threads = os.cpu_count() or 1
     probe = threads  # one series per thread, so the probe rate is the full-machine rate
     x = synth_random(probe, cfg["c"], cfg["l"], seed=seed).values
+    oracle_transform(x, bank, nthreads=threads)  # warm (library load, thread start-up)
     t0 = time.perf_counter()
     oracle_transform(x, bank, nthreads=threads)
     t_probe = time.perf_counter() - t0
