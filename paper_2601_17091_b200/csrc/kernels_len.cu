@@ -29,6 +29,18 @@ void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   }
 }
 
+// half-warp chunks (single channel): PPV/MAX kernels; MPV launches of these
+// classes run the full-warp MPV kernel on the same chunk data
+template <int RI, int P>
+void fill_half(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
+  constexpr int R = rk::r_of(RI);
+  wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, false, false, true>;
+  if constexpr (R <= rk::kExactRMax) {
+    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, true, false, false, true>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, true>;
+  }
+}
+
 // GMEM variants: every chunk uses the run-time slot layout; 2-pair chunks
 // at R <= 5, 1-pair chunks at any R — within registers.
 template <int RI, int P>
@@ -52,6 +64,8 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
   fill_wide<RI, 1, 2>(dt, mt, base + 1);
   fill_wide<RI, 1, 0>(dt, mt, base + 2);
   fill_wide<RI, 1, 1>(dt, mt, base + 3);
+  fill_half<RI, 2>(dt, mt, base + 4);
+  fill_half<RI, 1>(dt, mt, base + 5);
   fill_gmem<RI, 2>(gt, base + 0);
   fill_gmem<RI, 1>(gt, base + 1);
   fill_gmem<RI, 1>(gt, base + 2);

@@ -64,15 +64,17 @@ struct HostChunk {
 // (positions per lane, stride = dilation), following the kernel's lane map
 // (run_positions): full 32-lane steps of R positions, then 1-position
 // masked steps for the leftover positions.
-int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false) {
+// lanes = 16: half-warp chunks, whose steps serve two series (the caller
+// halves the step part).
+int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false, int lanes = 32) {
   const int64_t G = 2 * P;
   const int64_t RD = (int64_t)R * d;
   const int64_t A = n / RD;
   const int64_t rem = n - A * RD;
   const int64_t full_starts = A * d;
   const int64_t starts = full_starts + std::min<int64_t>(d, rem);
-  const int64_t nfull = full_starts / 32;
-  const int64_t masked_steps = (starts - nfull * 32 + 31) / 32;
+  const int64_t nfull = full_starts / lanes;
+  const int64_t masked_steps = (starts - nfull * lanes + lanes - 1) / lanes;
   auto step = [&](int64_t r, int64_t extra) {
     return r * len * nc * P              // FFMA2
            + r * G * 2                   // count (FSETP + IADD)
@@ -394,7 +396,11 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
       if (gnck == 0 && gri > 2) gc += (2 - gri) * rk::kNumNck;
       fn = kernel_table().gfn[2 * gc + exact];
     } else {
-      fn = fpk == 3 ? kernel_table().mfn[exec_cls(wl.cls, 1)] : kernel_table().dfn[2 * exec_cls(wl.cls, exact) + exact];
+      int cls = wl.cls;
+      // half-warp chunks need two series per item; otherwise run their data
+      // on the full-warp kernel of the same (length, R, pairs)
+      if (rk::nck_half(cls % rk::kNumNck) && spi < 2) cls += rk::nck_full(cls % rk::kNumNck) - cls % rk::kNumNck;
+      fn = fpk == 3 ? kernel_table().mfn[exec_cls(cls, 1)] : kernel_table().dfn[2 * exec_cls(cls, exact) + exact];
     }
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
     int rc = set_kernel_smem(st, (const void*)fn, smem * spi);
@@ -860,6 +866,12 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   // every chunk class runs on the wide kernel unless RK_NO_WIDE_PATH asks
   // for the class kernel (diagnostics)
   const bool wide_ok = !getenv("RK_NO_WIDE_PATH");
+  // half-warp chunks: wide path, staged series; chosen when the cost model
+  // says they beat the best full-warp R by the margin (percent, RK_HALF_MARGIN)
+  // (and only when a CTA can stage two series: otherwise items hold one
+  // series and the half classes would only add launches)
+  const bool half_ok = wide_ok && !gmem && !getenv("RK_NO_HALF") && 2 * smem + 1024 <= (int64_t)st->smem_optin;
+  const int64_t half_margin = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   std::vector<float> wpack;
   std::vector<int> chan_off;
   for (auto& kv : groups) {
@@ -906,6 +918,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       dc.invd = 1.0f / (float)d;
       int best_r = 0;
       int64_t best = INT64_MAX;
+      bool half = false;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
         if (nck == 2 && !wide_ok && ri != 0) continue;  // class-kernel generic path: 1 position per lane
         if (gmem && nck == 0 && ri > 2) continue;  // GMEM slot-loop kernels with 2 pairs: R <= 5 (registers)
@@ -913,8 +926,21 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
         if (cst < best) {
           best = cst;
           best_r = ri;
+          half = false;
+        }
+        // single-channel chunks may run as half-warp chunks (two series per
+        // pass of 16-lane steps): per series, half the 16-lane step cost
+        if (half_ok && nc == 1) {
+          const int64_t fixed = 40 * 2 * P + 60;
+          const int64_t c16 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 16) - fixed) / 2 + fixed;
+          if (c16 * 100 < best * half_margin) {
+            best = c16;
+            best_r = ri;
+            half = true;
+          }
         }
       }
+      if (half) nck = nck == 0 ? 4 : 5;
       hc.cost = best;
       dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
       // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is

@@ -62,7 +62,7 @@ constexpr unsigned kFull = 0xffffffffu;
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
 //           2: >= 3 channels, 1 pair (wide kernel: channel slots looped at
 //              run time; class kernel: the generic 1-position path);
-//           3: 1 channel, 1 pair
+//           3: 1 channel, 1 pair; 4 / 5: kinds 0 / 3 as half-warp chunks
 #ifndef RK_NUM_R
 #define RK_NUM_R 8
 #endif
@@ -78,10 +78,15 @@ __host__ __device__ constexpr int r_of(int r_idx) {
 constexpr int kExactRMax = 13;
 constexpr int kExactRIdx13 = 5;
 static_assert(r_of(kExactRIdx13) == kExactRMax, "R class table");
-constexpr int kNumNck = 4;
-// (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop
-__host__ __device__ constexpr int nck_pairs(int nck) { return nck == 0 ? 2 : 1; }
+constexpr int kNumNck = 6;
+// (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop.
+// 4 / 5: the 1-channel kinds 0 / 3 run as half-warp chunks (two series per
+// pass); same chunk data, so they fall back to 0 / 3 when items hold one
+// series.
+__host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4) ? 2 : 1; }
 __host__ __device__ constexpr int nck_slots(int nck) { return nck == 1 ? 2 : nck == 2 ? 0 : 1; }
+__host__ __device__ constexpr bool nck_half(int nck) { return nck >= 4; }
+__host__ __device__ constexpr int nck_full(int nck) { return nck == 4 ? 0 : nck == 5 ? 3 : nck; }
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
 // One chunk (class-kernel layout, global memory).
@@ -322,6 +327,47 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G, MPV>& st, floa
   }
 }
 
+// Finish for half-warp chunks: lanes 0-15 hold series A's pools, 16-31
+// series B's; butterfly reductions inside each half, then lane g of each
+// half writes kernel g of its series (orow_b may be null: no second series).
+template <int G, bool EXACT, class CH>
+__device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G>& st, float* __restrict__ orow_a,
+                                                  float* __restrict__ orow_b, int fpk, int vec_out, int lane) {
+  const int hl = lane & 15;
+  unsigned my_cnt = 0;
+  float my_ext = 0.0f, my_bias = 0.0f;
+  int my_col = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    unsigned cnt = st.cnt[g];
+    float e = st.ext[g];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, o);
+      const float oe = __shfl_xor_sync(kFull, e, o);
+      e = EXACT ? fmaxf(e, oe) : fminf(e, oe);
+    }
+    if (hl == g) {
+      my_cnt = cnt;
+      my_ext = e;
+      my_bias = c.bias[g];
+      my_col = c.col[g];
+    }
+  }
+  float* orow = lane < 16 ? orow_a : orow_b;
+  if (hl < c.nk && orow) {
+    const float ppv = __fdiv_rn((float)my_cnt, (float)c.n);  // == f32(RN64(count / l_out)), see finish_chunk
+    const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
+    float* dst = orow + (int64_t)my_col * fpk;
+    if (vec_out) {
+      *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
+    } else {
+      dst[0] = ppv;
+      dst[1] = mx;
+    }
+  }
+}
+
 // One step: R positions per lane (u0, u0+d, ..., u0+(R-1)d) for P kernel
 // pairs over NC channel slots.
 template <int LEN, int R, int P, int NC, bool EXACT, bool MASKED, bool MPV = false>
@@ -357,17 +403,20 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P, MPV>& st, const float* co
 // all complete runs go through the unmasked path; the remaining starts
 // (an incomplete 32-group and the final partial run, whose positions
 // v0 + r*d may pass n) through masked steps with clamped reads.
-template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false>
+// LANES = 16: a half-warp walks one series (lane is the lane in the half,
+// q32 / r32 are 16 / d and 16 % d).
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, int LANES = 32>
 __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
                                               int r32, float invd, const float* nan_slot, int lane) {
+  constexpr int kLog = LANES == 32 ? 5 : 4;
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
   const int full_starts = A * d;
   const int starts = full_starts + min(d, rem);
-  const int nfull = full_starts >> 5;
+  const int nfull = full_starts >> kLog;
   // (a, s) = divmod(32*step + lane, d), advanced incrementally; the first
   // divmod of lane < 32 is exact in float ((lane + 0.5) / d is never within
   // 2^-20 of an integer)
@@ -385,7 +434,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
       v0 += RD - d;
     }
   }
-  for (int base = nfull << 5; base < starts; base += 32) {
+  for (int base = nfull << kLog; base < starts; base += LANES) {
     const bool live = base + lane < starts;
     chunk_step<LEN, R, P, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
                                            live ? n - v0 : 0, nan_slot);
@@ -985,7 +1034,7 @@ __device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned 
                : "memory");
 }
 
-template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false>
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false, bool HALF = false>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
@@ -1081,6 +1130,30 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           for (int q = 0; q < P; ++q)
 #pragma unroll
             for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
+        if constexpr (HALF) {
+          // half-warp chunks: two series per pass, 16 lanes each (finer
+          // step granularity for short position ranges); an odd last series
+          // is shadowed by the upper half, which writes nothing
+          static_assert(!MPV && !GMEM, "half-warp chunks: PPV/MAX on staged series");
+          const int half = lane >> 4, hl = lane & 15;
+          const int q16 = c.q32 >> 1, r16 = 16 - q16 * c.d;
+          for (int si = 0; si < ns; si += 2) {
+            const int sj = min(si + half, ns - 1);
+            const float* sx = sbase + sj * slot + H;
+            const float* chan[NC];
+#pragma unroll
+            for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+            Pool<2 * P> st;
+            pool_init<2 * P, EXACT>(st);
+            run_positions<LEN, R, P, NC, EXACT, false, 16>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, q16, r16,
+                                                           c.invd, nanp, hl);
+            float* orow_a = p.h.out + (series0 + si) * p.h.ld_out;
+            finish_chunk_half<2 * P, EXACT>(c, st, orow_a, si + 1 < ns ? orow_a + p.h.ld_out : nullptr, p.h.fpk,
+                                            p.h.vec_out, lane);
+            done += (unsigned long long)c.nk * (unsigned long long)c.n * (si + 1 < ns ? 2u : 1u);
+          }
+          continue;
+        }
         // the chunk's weights serve every staged series of the item
         for (int si = 0; si < ns; ++si) {
           const float* sx = sbase + si * slot + H;

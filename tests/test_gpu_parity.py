@@ -337,3 +337,18 @@ def test_concurrent_callers_on_one_stream(cuda_ready):
     for i, x in enumerate(xs):
         assert outs[i].cpu().numpy().tobytes() == ref[i].tobytes()
         assert executed[i] == expected_dot_products(bank, x.shape[0])
+
+
+@pytest.mark.parametrize("n", [3601, 9000])
+def test_half_warp_chunks_exact(n, cuda_ready):
+    """Enough series for two-series items, so the single-channel chunks run
+    as half-warp chunks (16 lanes per series; an odd last series shadowed by
+    the upper half): bytes equal to the oracle on every row, fast mode within
+    tolerance."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(256, 1, 300, GenOptions(seed=77))
+    values = synth_random(n, 1, 256, seed=78).values
+    ref = oracle_transform(values, bank)
+    assert transform(values, bank, mode="exact").values.tobytes() == ref.tobytes()
+    check_fast(transform(values, bank, mode="fast").values, ref, values, bank)
