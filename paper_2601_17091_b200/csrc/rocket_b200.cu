@@ -1251,7 +1251,8 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
   batch = std::min<int64_t>(batch, n);
   // several batches when there is enough work to overlap the copies
   const int64_t nbatch_min = getenv("RK_E2E_BATCHES") ? std::max(1, atoi(getenv("RK_E2E_BATCHES"))) : 6;
-  if (n >= 4096) batch = std::min<int64_t>(batch, (n + nbatch_min - 1) / nbatch_min);
+  const int64_t min_rows = getenv("RK_E2E_MIN_ROWS") ? std::max(1, atoi(getenv("RK_E2E_MIN_ROWS"))) : 4096;
+  if (n >= min_rows) batch = std::min<int64_t>(batch, (n + nbatch_min - 1) / nbatch_min);
   if (!dx) {
     const size_t need = (size_t)(batch * in_row_bytes);
     if (need > w->in_cap) {
