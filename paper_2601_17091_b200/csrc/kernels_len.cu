@@ -29,15 +29,14 @@ void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   }
 }
 
-// half-warp chunks (single channel): PPV/MAX kernels; MPV launches of these
-// classes run the full-warp MPV kernel on the same chunk data
+// half-warp chunks (single channel): PPV/MAX kernels and the fast MPV kernel
 template <int RI, int P>
 void fill_half(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   constexpr int R = rk::r_of(RI);
   wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, false, false, true>;
   if constexpr (R <= rk::kExactRMax) {
     wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, true, false, false, true>;
-    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, true>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, true, false, true>;
   }
 }
 

@@ -330,28 +330,32 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G, MPV>& st, floa
 // Finish for half-warp chunks: lanes 0-15 hold series A's pools, 16-31
 // series B's; butterfly reductions inside each half, then lane g of each
 // half writes kernel g of its series (orow_b may be null: no second series).
-template <int G, bool EXACT, class CH>
-__device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G>& st, float* __restrict__ orow_a,
+template <int G, bool EXACT, class CH, bool MPV = false>
+__device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G, MPV>& st, float* __restrict__ orow_a,
                                                   float* __restrict__ orow_b, int fpk, int vec_out, int lane) {
   const int hl = lane & 15;
   unsigned my_cnt = 0;
-  float my_ext = 0.0f, my_bias = 0.0f;
+  float my_ext = 0.0f, my_bias = 0.0f, my_ps = 0.0f;
   int my_col = 0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     unsigned cnt = st.cnt[g];
     float e = st.ext[g];
+    float ps = 0.0f;
+    if (MPV) ps = (g & 1) ? st.ps[g / 2].y : st.ps[g / 2].x;
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
       cnt += __shfl_xor_sync(kFull, cnt, o);
       const float oe = __shfl_xor_sync(kFull, e, o);
       e = EXACT ? fmaxf(e, oe) : fminf(e, oe);
+      if (MPV) ps += __shfl_xor_sync(kFull, ps, o);
     }
     if (hl == g) {
       my_cnt = cnt;
       my_ext = e;
       my_bias = c.bias[g];
       my_col = c.col[g];
+      my_ps = ps;
     }
   }
   float* orow = lane < 16 ? orow_a : orow_b;
@@ -365,6 +369,7 @@ __device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G>& st, floa
       dst[0] = ppv;
       dst[1] = mx;
     }
+    if (MPV) dst[2] = my_cnt ? __double2float_rn((double)(-my_ps) / (double)my_cnt) : 0.0f;  // see finish_chunk
   }
 }
 
@@ -1134,7 +1139,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           // half-warp chunks: two series per pass, 16 lanes each (finer
           // step granularity for short position ranges); an odd last series
           // is shadowed by the upper half, which writes nothing
-          static_assert(!MPV && !GMEM, "half-warp chunks: PPV/MAX on staged series");
+          static_assert(!GMEM && !(MPV && EXACT), "half-warp chunks: staged series; MPV in fast mode");
           const int half = lane >> 4, hl = lane & 15;
           const int q16 = c.q32 >> 1, r16 = 16 - q16 * c.d;
           for (int si = 0; si < ns; si += 2) {
@@ -1143,13 +1148,13 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             const float* chan[NC];
 #pragma unroll
             for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
-            Pool<2 * P> st;
-            pool_init<2 * P, EXACT>(st);
-            run_positions<LEN, R, P, NC, EXACT, false, 16>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, q16, r16,
-                                                           c.invd, nanp, hl);
+            Pool<2 * P, MPV> st;
+            pool_init<2 * P, EXACT, MPV>(st);
+            run_positions<LEN, R, P, NC, EXACT, MPV, 16>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, q16, r16,
+                                                         c.invd, nanp, hl);
             float* orow_a = p.h.out + (series0 + si) * p.h.ld_out;
-            finish_chunk_half<2 * P, EXACT>(c, st, orow_a, si + 1 < ns ? orow_a + p.h.ld_out : nullptr, p.h.fpk,
-                                            p.h.vec_out, lane);
+            finish_chunk_half<2 * P, EXACT, WChunk, MPV>(c, st, orow_a, si + 1 < ns ? orow_a + p.h.ld_out : nullptr,
+                                                         p.h.fpk, p.h.vec_out, lane);
             done += (unsigned long long)c.nk * (unsigned long long)c.n * (si + 1 < ns ? 2u : 1u);
           }
           continue;

@@ -343,8 +343,8 @@ def test_concurrent_callers_on_one_stream(cuda_ready):
 def test_half_warp_chunks_exact(n, cuda_ready):
     """Enough series for two-series items, so the single-channel chunks run
     as half-warp chunks (16 lanes per series; an odd last series shadowed by
-    the upper half): bytes equal to the oracle on every row, fast mode within
-    tolerance."""
+    the upper half): bytes equal to the oracle on every row, fast mode (with
+    and without MPV) within tolerance."""
     from oracle.oracle import oracle_transform
 
     bank = generate_bank(256, 1, 300, GenOptions(seed=77))
@@ -352,3 +352,5 @@ def test_half_warp_chunks_exact(n, cuda_ready):
     ref = oracle_transform(values, bank)
     assert transform(values, bank, mode="exact").values.tobytes() == ref.tobytes()
     check_fast(transform(values, bank, mode="fast").values, ref, values, bank)
+    ref3 = oracle_transform(values, bank, include_mpv=True)
+    check_fast(transform(values, bank, include_mpv=True, mode="fast").values, ref3, values, bank, fpk=3)
