@@ -868,9 +868,16 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   const bool wide_ok = !getenv("RK_NO_WIDE_PATH");
   // half-warp chunks: wide path, staged series; chosen when the cost model
   // says they beat the best full-warp R by the margin (percent, RK_HALF_MARGIN)
-  // (and only when a CTA can stage two series: otherwise items hold one
-  // series and the half classes would only add launches)
-  const bool half_ok = wide_ok && !gmem && !getenv("RK_NO_HALF") && 2 * smem + 1024 <= (int64_t)st->smem_optin;
+  // (and only when the wide path's CTAs can stage two series each at the
+  // CTA count they will run at — launch_wide_chain's series-per-item rule —
+  // otherwise items hold one series and the half classes would only run
+  // their chunks on the full-warp kernel at an R priced for 16 lanes: 3
+  // channels x L = 2048, 4 CTAs per SM, measured 0.4 % / 1.3 % slower)
+  const int half_ctas = std::min<int>(
+      std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))),
+      getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6);
+  const bool half_ok = wide_ok && !gmem && !getenv("RK_NO_HALF") &&
+                       (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   const int64_t half_margin = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   std::vector<float> wpack;
   std::vector<int> chan_off;
