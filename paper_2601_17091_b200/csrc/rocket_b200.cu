@@ -135,8 +135,12 @@ struct rk_bank_s {
   int64_t device_bytes = 0;
   std::map<std::pair<int, int>, int*> d_block_start;  // (class, n_blocks) -> device boundaries
   std::mutex mu;
+  // the same bank without half-warp chunks, for transforms whose items hold
+  // one series (null when the bank has no half-warp chunks)
+  rk_bank_s* full_bank = nullptr;
 
   ~rk_bank_s() {
+    delete full_bank;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
@@ -368,7 +372,6 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   static const bool profile = getenv("RK_PROFILE") != nullptr;
   static rk::WParams params;  // 32 KB: kept off the stack; guarded by the caller's lock
   static std::mutex params_mu;
-  std::lock_guard<std::mutex> lk(params_mu);
   const int smem = b->gmem ? 0 : b->smem_bytes;
   // Few series: more, narrower CTAs (down to one warp) so every SM still has
   // work; many series: wide_ctas_per_sm CTAs of 24/ctas warps.
@@ -383,6 +386,12 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   while (spi < spi_max && n >= min_items * (spi + 1) * st->sms * ctas &&
          (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
     ++spi;
+  // one series per item: half-warp chunks cannot pair series, so run the
+  // bank's full-warp twin
+  if (spi < 2 && b->full_bank)
+    return launch_wide_chain(b->full_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
+                             nanp);
+  std::lock_guard<std::mutex> lk(params_mu);
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
@@ -772,10 +781,13 @@ int rk_device_count(int32_t* count) {
   return RK_OK;
 }
 
-int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
-                   const int32_t* paddings, const float* biases, const float* weights,
-                   const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
-                   int32_t device, rk_bank_t* out) {
+namespace {
+// allow_half = false builds the layout without half-warp chunks (the
+// full-warp twin of a bank, see rk_bank_s::full_bank).
+int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
+                     const int32_t* paddings, const float* biases, const float* weights, const int64_t* woff,
+                     const int32_t* chidx, const int64_t* choff, const int32_t* chcnt, int32_t device,
+                     bool allow_half, rk_bank_t* out) {
   if (!out) return fail(RK_ERR_INVALID, "bank output pointer is NULL");
   *out = nullptr;
   if (K < 1) return fail(RK_ERR_INVALID, "bank must contain at least one kernel");
@@ -876,7 +888,7 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   const int half_ctas = std::min<int>(
       std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))),
       getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6);
-  const bool half_ok = wide_ok && !gmem && !getenv("RK_NO_HALF") &&
+  const bool half_ok = allow_half && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   const int64_t half_margin = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   std::vector<float> wpack;
@@ -1157,6 +1169,34 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   b->device_bytes = (int64_t)(sizeof(rk::DevChunk) * dev.size() + sizeof(float) * wpack.size() +
                               sizeof(int) * chan_off.size());
   *out = b.release();
+  return RK_OK;
+}
+}  // namespace
+
+int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
+                   const int32_t* paddings, const float* biases, const float* weights,
+                   const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
+                   int32_t device, rk_bank_t* out) {
+  int rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
+                            true, out);
+  if (rc) return rc;
+  rk_bank_t b = *out;
+  bool has_half = false;
+  for (const auto& wl : b->wide_launches) has_half |= rk::nck_half(wl.cls % rk::kNumNck);
+  if (has_half) {
+    // Transforms whose items hold one series (few series) run the full-warp
+    // twin: half-warp chunks there would run on the full-warp kernel at an
+    // R priced for 16 lanes (config 2 bank at 2,000 series: -6 % fast,
+    // -11 % exact).
+    rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
+                          false, &b->full_bank);
+    if (rc) {
+      delete b;
+      *out = nullptr;
+      return rc;
+    }
+    b->device_bytes += b->full_bank->device_bytes;
+  }
   return RK_OK;
 }
 
