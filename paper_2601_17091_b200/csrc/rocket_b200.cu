@@ -138,9 +138,13 @@ struct rk_bank_s {
   // the same bank without half-warp chunks, for transforms whose items hold
   // one series (null when the bank has no half-warp chunks)
   rk_bank_s* full_bank = nullptr;
+  // the same bank with the exact-mode half-warp margin (null when equal to
+  // the fast-mode layout's or without half-warp chunks)
+  rk_bank_s* exact_bank = nullptr;
 
   ~rk_bank_s() {
     delete full_bank;
+    delete exact_bank;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
@@ -390,6 +394,10 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   // bank's full-warp twin
   if (spi < 2 && b->full_bank)
     return launch_wide_chain(b->full_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
+                             nanp);
+  // exact mode: the layout priced with its own half-warp margin
+  if (exact && fpk == 2 && b->exact_bank)
+    return launch_wide_chain(b->exact_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
   std::lock_guard<std::mutex> lk(params_mu);
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
@@ -782,12 +790,13 @@ int rk_device_count(int32_t* count) {
 }
 
 namespace {
-// allow_half = false builds the layout without half-warp chunks (the
-// full-warp twin of a bank, see rk_bank_s::full_bank).
+// half_margin (percent): a chunk runs half-warp when its modelled cost is
+// below half_margin % of the best full-warp option; 0 builds the layout
+// without half-warp chunks (the full-warp twin, rk_bank_s::full_bank).
 int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
                      const int32_t* paddings, const float* biases, const float* weights, const int64_t* woff,
                      const int32_t* chidx, const int64_t* choff, const int32_t* chcnt, int32_t device,
-                     bool allow_half, rk_bank_t* out) {
+                     int64_t half_margin, rk_bank_t* out) {
   if (!out) return fail(RK_ERR_INVALID, "bank output pointer is NULL");
   *out = nullptr;
   if (K < 1) return fail(RK_ERR_INVALID, "bank must contain at least one kernel");
@@ -888,9 +897,8 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   const int half_ctas = std::min<int>(
       std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))),
       getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6);
-  const bool half_ok = allow_half && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
+  const bool half_ok = half_margin > 0 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
-  const int64_t half_margin = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   std::vector<float> wpack;
   std::vector<int> chan_off;
   for (auto& kv : groups) {
@@ -1177,25 +1185,45 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
                    const int32_t* paddings, const float* biases, const float* weights,
                    const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
                    int32_t device, rk_bank_t* out) {
+  // the half-warp margin of the cost model, per mode (measured optima:
+  // profiles/r01_half_margin_sweep.txt)
+  const int64_t margin_fast = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
+  const int64_t margin_exact = getenv("RK_HALF_MARGIN_EXACT") ? atoi(getenv("RK_HALF_MARGIN_EXACT")) : 110;
   int rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
-                            true, out);
+                            margin_fast, out);
   if (rc) return rc;
   rk_bank_t b = *out;
-  bool has_half = false;
-  for (const auto& wl : b->wide_launches) has_half |= rk::nck_half(wl.cls % rk::kNumNck);
-  if (has_half) {
+  auto has_half = [](rk_bank_t x) {
+    for (const auto& wl : x->wide_launches)
+      if (rk::nck_half(wl.cls % rk::kNumNck)) return true;
+    return false;
+  };
+  auto twin = [&](int64_t margin, rk_bank_t* dst) -> int {
+    int r = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt,
+                             device, margin, dst);
+    if (r) {
+      delete b;
+      *out = nullptr;
+      return r;
+    }
+    b->device_bytes += (*dst)->device_bytes;
+    return RK_OK;
+  };
+  if (has_half(b)) {
     // Transforms whose items hold one series (few series) run the full-warp
     // twin: half-warp chunks there would run on the full-warp kernel at an
     // R priced for 16 lanes (config 2 bank at 2,000 series: -6 % fast,
     // -11 % exact).
-    rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
-                          false, &b->full_bank);
-    if (rc) {
-      delete b;
-      *out = nullptr;
-      return rc;
+    if ((rc = twin(0, &b->full_bank))) return rc;
+    // exact mode (FMUL2 + FFMA2 per tap) favours half-warp chunks more
+    if (margin_exact != margin_fast) {
+      if ((rc = twin(margin_exact, &b->exact_bank))) return rc;
+      if (!has_half(b->exact_bank)) {
+        b->device_bytes -= b->exact_bank->device_bytes;
+        delete b->exact_bank;
+        b->exact_bank = nullptr;
+      }
     }
-    b->device_bytes += b->full_bank->device_bytes;
   }
   return RK_OK;
 }
