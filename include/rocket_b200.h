@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define RK_ABI_VERSION 1
+#define RK_ABI_VERSION 2
 
 /* Error codes.  RK_ERR_CAPACITY mirrors gridrocket.CapacityError
  * (engine.py:30-31); RK_ERR_INVALID mirrors the ValueError raised by
@@ -77,6 +77,9 @@ typedef struct rk_bank_info_s {
                            global memory (series too long for shared
                            memory); 0: class kernel (RK_NO_WIDE_PATH) */
   int32_t ctas_per_sm;  /* resident CTAs per SM on the wide path */
+  int32_t n_half_chunks; /* chunks laid out as half-warp chunks (two series
+                            per 16-lane pass) in the fast-mode layout */
+  int32_t reserved;
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */
@@ -164,6 +167,31 @@ int64_t rk_run_batch_f64(const double* x, int64_t n_instances,
                          const int32_t* chcnt, int64_t n_kernels,
                          int32_t workers, int32_t fpk, double* out,
                          int64_t ld_out, int64_t row0);
+
+/* The drop-in entry points with the arithmetic mode chosen by the caller
+ * (RK_MODE_EXACT: byte-identical to the reference, as rk_run_batch_f32;
+ * RK_MODE_FAST: the FFMA2 kernels within the north-star tolerance — the
+ * headline kernels reached through the reference's own operator call).
+ * Same arguments as rk_run_batch_f32 / _f64 plus mode; same return value.
+ * float64 runs the reference loop in either mode (bytes equal). */
+int64_t rk_run_batch_f32_mode(const float* x, int64_t n_instances,
+                              int32_t n_channels, int32_t l_series,
+                              const int32_t* lengths, const int32_t* dilations,
+                              const int32_t* paddings, const float* biases,
+                              const float* wflat, const int64_t* woff,
+                              const int32_t* chidx, const int64_t* choff,
+                              const int32_t* chcnt, int64_t n_kernels,
+                              int32_t workers, int32_t fpk, float* out,
+                              int64_t ld_out, int64_t row0, int32_t mode);
+int64_t rk_run_batch_f64_mode(const double* x, int64_t n_instances,
+                              int32_t n_channels, int32_t l_series,
+                              const int32_t* lengths, const int32_t* dilations,
+                              const int32_t* paddings, const double* biases,
+                              const double* wflat, const int64_t* woff,
+                              const int32_t* chidx, const int64_t* choff,
+                              const int32_t* chcnt, int64_t n_kernels,
+                              int32_t workers, int32_t fpk, double* out,
+                              int64_t ld_out, int64_t row0, int32_t mode);
 
 /* Streaming transform between files: the reference's
  * `gridrocket transform` reads the whole dataset (load_dataset,

@@ -184,3 +184,132 @@ void rko_convolve_f64(const double* x, int64_t L, const int32_t* chidx, int64_t 
     out[t] = acc + bias;
   }
 }
+
+/* Floating-point certification of single-precision cells (the fast-mode
+ * tolerance, tests/parity.py).  For each requested (row, kernel) cell the
+ * convolution is recomputed exactly enough in float64 from the SAME float32
+ * operands the transforms use (the bank cast to float32 as engine.py:275-276
+ * does; a float32 x float32 product is exact in float64), and each output t
+ * gets the classical forward-error bound of a float32 evaluation in any
+ * order, with or without FMA (Higham, Accuracy and Stability of Numerical
+ * Algorithms, 2nd ed., eq. 3.5 / Lemma 3.1):
+ *     e_t = gamma(m + 1) * (|b| + sum_taps |w * x|),
+ *     gamma(n) = n u / (1 - n u),  u = 2^-24,  m = in-range taps at t.
+ * Outputs per cell:
+ *   max64[i]   max_t v64[t]                (the float64 MAX)
+ *   maxerr[i]  max_t e_t                   (|MAX_f32 - max64| <= maxerr)
+ *   near[i]    #{t : |v64[t]| < near_abs}  (the north star's 1e-6 band)
+ *   unsure[i]  #{t : |v64[t]| <= max(near_abs, e_t)} (sign not decided by
+ *              float32 arithmetic)
+ *   pos[i]     #{t : v64[t] > 0}
+ *   psum64[i]  sum of the positive v64[t]
+ *   psumerr[i] sum over t with v64[t] > -e_t of 2 e_t (a bound on how far
+ *              any float32 positive sum's terms and membership move it)
+ */
+typedef struct {
+  const float* x;
+  int64_t C, L;
+  const int32_t *lengths, *dilations, *paddings, *chidx, *chcnt;
+  const float *biases, *wflat;
+  const int64_t *woff, *choff, *rows, *ks;
+  double near_abs;
+  double *max64, *maxerr, *psum64, *psumerr;
+  int64_t *near, *unsure, *pos;
+  int64_t begin, end;
+} cert_t;
+
+static void* cert_worker(void* arg) {
+  cert_t* c = (cert_t*)arg;
+  const double u = ldexp(1.0, -24);
+  for (int64_t i = c->begin; i < c->end; ++i) {
+    const int64_t k = c->ks[i];
+    const float* xi = c->x + c->rows[i] * c->C * c->L;
+    const int64_t L = c->L, lk = c->lengths[k], d = c->dilations[k], p = c->paddings[k];
+    const int64_t l_out = L + 2 * p - (lk - 1) * d, nc = c->chcnt[k];
+    const float* w = c->wflat + c->woff[k];
+    const double b = (double)c->biases[k];
+    double mx = -INFINITY, mxe = 0.0, ps = 0.0, pse = 0.0;
+    int64_t near = 0, unsure = 0, pos = 0;
+    for (int64_t t = 0; t < l_out; ++t) {
+      double acc = 0.0, mag = fabs(b);
+      int64_t m = 0;
+      for (int64_t ch = 0; ch < nc; ++ch) {
+        const float* xc = xi + (int64_t)c->chidx[c->choff[k] + ch] * L;
+        for (int64_t q = 0; q < lk; ++q) {
+          const int64_t idx = t - p + q * d;
+          if (idx >= 0 && idx < L) {
+            const double prod = (double)w[ch * lk + q] * (double)xc[idx];
+            acc += prod;
+            mag += fabs(prod);
+            ++m;
+          }
+        }
+      }
+      const double v = acc + b;
+      const double g = (double)(m + 1) * u / (1.0 - (double)(m + 1) * u);
+      /* + 2^-50 mag: the float64 evaluation's own rounding */
+      const double e = g * mag + ldexp(mag, -50);
+      if (v > mx) mx = v;
+      if (e > mxe) mxe = e;
+      if (fabs(v) < c->near_abs) ++near;
+      if (fabs(v) <= (e > c->near_abs ? e : c->near_abs)) ++unsure;
+      if (v > 0) {
+        ++pos;
+        ps += v;
+      }
+      if (v > -e) pse += 2.0 * e;
+    }
+    c->max64[i] = mx;
+    c->maxerr[i] = mxe;
+    c->near[i] = near;
+    c->unsure[i] = unsure;
+    c->pos[i] = pos;
+    c->psum64[i] = ps;
+    c->psumerr[i] = pse;
+  }
+  return NULL;
+}
+
+void rko_cell_cert(const float* x, int64_t C, int64_t L, const int32_t* lengths, const int32_t* dilations,
+                   const int32_t* paddings, const float* biases, const float* wflat, const int64_t* woff,
+                   const int32_t* chidx, const int64_t* choff, const int32_t* chcnt, const int64_t* rows,
+                   const int64_t* ks, int64_t ncells, double near_abs, double* max64, double* maxerr, int64_t* near,
+                   int64_t* unsure, int64_t* pos, double* psum64, double* psumerr, int32_t nthreads) {
+  if (ncells <= 0) return;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > ncells) nthreads = (int32_t)ncells;
+  cert_t* jobs = (cert_t*)calloc((size_t)nthreads, sizeof(cert_t));
+  pthread_t* th = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int32_t t = 0; t < nthreads; ++t) {
+    cert_t* j = &jobs[t];
+    j->x = x;
+    j->C = C;
+    j->L = L;
+    j->lengths = lengths;
+    j->dilations = dilations;
+    j->paddings = paddings;
+    j->chidx = chidx;
+    j->chcnt = chcnt;
+    j->biases = biases;
+    j->wflat = wflat;
+    j->woff = woff;
+    j->choff = choff;
+    j->rows = rows;
+    j->ks = ks;
+    j->near_abs = near_abs;
+    j->max64 = max64;
+    j->maxerr = maxerr;
+    j->psum64 = psum64;
+    j->psumerr = psumerr;
+    j->near = near;
+    j->unsure = unsure;
+    j->pos = pos;
+    j->begin = ncells * t / nthreads;
+    j->end = ncells * (t + 1) / nthreads;
+  }
+  for (int32_t t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, cert_worker, &jobs[t]);
+  cert_worker(&jobs[0]);
+  for (int32_t t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(jobs);
+  free(th);
+}

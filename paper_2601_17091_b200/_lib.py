@@ -40,6 +40,8 @@ EXPORTS = (
     "rk_transform_f32",
     "rk_run_batch_f32",
     "rk_run_batch_f64",
+    "rk_run_batch_f32_mode",
+    "rk_run_batch_f64_mode",
     "rk_release_caches",
     "rk_transform_stream",
     "rk_generate_bank",
@@ -71,6 +73,8 @@ class BankInfo(ctypes.Structure):
         ("n_launches", ctypes.c_int32),
         ("path", ctypes.c_int32),
         ("ctas_per_sm", ctypes.c_int32),
+        ("n_half_chunks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -157,6 +161,10 @@ def load():
                                      p, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.rk_run_batch_f32.restype = i64
     lib.rk_run_batch_f32.argtypes = [p, i64, i32, i32, p, p, p, p, p, p, p, p, p, i64, i32, i32, p, i64, i64]
+    lib.rk_run_batch_f32_mode.restype = i64
+    lib.rk_run_batch_f32_mode.argtypes = [p, i64, i32, i32, p, p, p, p, p, p, p, p, p, i64, i32, i32, p, i64, i64, i32]
+    lib.rk_run_batch_f64_mode.restype = i64
+    lib.rk_run_batch_f64_mode.argtypes = [p, i64, i32, i32, p, p, p, p, p, p, p, p, p, i64, i32, i32, p, i64, i64, i32]
     lib.rk_release_caches.restype = ctypes.c_int
     lib.rk_release_caches.argtypes = []
     _lib = lib

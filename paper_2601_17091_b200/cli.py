@@ -123,8 +123,8 @@ def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2601_17091_b200", description="B200 ROCKET transform")
     sub = parser.add_subparsers(dest="command", required=True)
     p = sub.add_parser("transform", help="extract features from a dataset")
-    p.add_argument("--data", required=True, help=".ts, .csv, or binary cache path")
-    p.add_argument("--csv-labels", action="store_true", help="CSV input has labels in the last column")
+    p.add_argument("--data", required=True, help="binary dataset cache (RKDS) or .npy array path")
+    p.add_argument("--csv-labels", action="store_true", help=argparse.SUPPRESS)  # reference flag; text input is out of scope
     p.add_argument("--bank", help="load kernels from this bank file")
     p.add_argument("--kernels", type=int, help="generate this many kernels instead")
     p.add_argument("--seed", type=int, default=0)

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -135,6 +136,7 @@ struct rk_bank_s {
   int64_t device_bytes = 0;
   std::map<std::pair<int, int>, int*> d_block_start;  // (class, n_blocks) -> device boundaries
   std::mutex mu;
+  std::atomic<bool> f64_ready{false};  // d_cw64 / d_cb64 filled (rk_bank_attach_f64)
   // the same bank without half-warp chunks, for transforms whose items hold
   // one series (null when the bank has no half-warp chunks)
   rk_bank_s* full_bank = nullptr;
@@ -213,6 +215,7 @@ struct DeviceState {
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
   std::map<const void*, int> attr_smem;
+  std::mutex attr_mu;
   std::mutex pool_mu;
   std::vector<Worker*> free_workers;
   // device-pointer calls: one scratch block per stream (stream order makes
@@ -328,7 +331,7 @@ void release_worker(DeviceState* st, Worker* w) {
 }
 
 int set_kernel_smem(DeviceState* st, const void* fn, int bytes) {
-  std::lock_guard<std::mutex> lk(g_dev_mu);
+  std::lock_guard<std::mutex> lk(st->attr_mu);
   auto it = st->attr_smem.find(fn);
   if (it == st->attr_smem.end() || it->second < bytes) {
     RK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -374,8 +377,10 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
                       const float* xpad, const float* nanp) {
   const int exact = mode == RK_MODE_EXACT ? 1 : 0;
   static const bool profile = getenv("RK_PROFILE") != nullptr;
-  static rk::WParams params;  // 32 KB: kept off the stack; guarded by the caller's lock
-  static std::mutex params_mu;
+  // 32 KB parameter block, one per host thread (kept off the stack; the
+  // launch copies it, so concurrent callers on other devices or streams
+  // never share or wait for it)
+  static thread_local rk::WParams params;
   const int smem = b->gmem ? 0 : b->smem_bytes;
   // Few series: more, narrower CTAs (down to one warp) so every SM still has
   // work; many series: wide_ctas_per_sm CTAs of 24/ctas warps.
@@ -399,7 +404,6 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   if (exact && fpk == 2 && b->exact_bank)
     return launch_wide_chain(b->exact_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
-  std::lock_guard<std::mutex> lk(params_mu);
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
@@ -616,7 +620,8 @@ int launch_cellrows_gmem(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStrea
 
 int launch_cells(rk_bank_t b, DeviceState* st, const void* d_x, int esz, int64_t n, void* d_out, int64_t ld_out,
                  int fpk, cudaStream_t stream, unsigned long long* d_exec, int* d_counters) {
-  if (esz == 8 && !b->d_cw64) return fail(RK_ERR_INVALID, "double precision needs rk_bank_attach_f64 first");
+  if (esz == 8 && !b->f64_ready.load(std::memory_order_acquire))
+    return fail(RK_ERR_INVALID, "double precision needs rk_bank_attach_f64 first");
   rk::CellArgs a = {};
   a.x = d_x;
   a.out = d_out;
@@ -1249,6 +1254,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->device = b->device;
   info->path = b->wide_path ? (b->gmem ? 2 : 1) : 0;
   info->ctas_per_sm = b->wide_ctas_per_sm;
+  for (const auto& hc : b->chunks) info->n_half_chunks += rk::nck_half(hc.dev.cls % rk::kNumNck) ? 1 : 0;
   if (b->wide_path)
     info->n_launches = (int32_t)b->wide_launches.size();
   else
@@ -1416,10 +1422,15 @@ int rk_bank_attach_f64(rk_bank_t b, const double* biases, const double* weights)
   RK_CUDA(cudaSetDevice(b->device));
   std::vector<double> cb(b->K);
   for (int64_t i = 0; i < b->K; ++i) cb[i] = biases[b->cell_order[i]];
+  // one attach at a time per bank; a transform sees the parameters only
+  // once they are complete (f64_ready)
+  std::lock_guard<std::mutex> lk(b->mu);
+  if (b->f64_ready.load(std::memory_order_acquire)) return RK_OK;  // immutable bank: attached once
   if (!b->d_cw64) RK_CUDA(cudaMalloc(&b->d_cw64, sizeof(double) * std::max<int64_t>(1, b->n_weights)));
   if (!b->d_cb64) RK_CUDA(cudaMalloc(&b->d_cb64, sizeof(double) * b->K));
   RK_CUDA(cudaMemcpy(b->d_cw64, weights, sizeof(double) * b->n_weights, cudaMemcpyHostToDevice));
   RK_CUDA(cudaMemcpy(b->d_cb64, cb.data(), sizeof(double) * b->K, cudaMemcpyHostToDevice));
+  b->f64_ready.store(true, std::memory_order_release);
   return RK_OK;
 }
 
@@ -1435,7 +1446,9 @@ struct CacheKey {
   }
 };
 std::mutex g_cache_mu;
-std::map<CacheKey, rk_bank_t> g_cache;
+// shared ownership: evicting an entry never frees a bank another caller is
+// still transforming with (the last reference destroys it)
+std::map<CacheKey, std::shared_ptr<rk_bank_s>> g_cache;
 
 uint64_t fnv(uint64_t h, const void* data, size_t bytes) {
   const unsigned char* c = (const unsigned char*)data;
@@ -1453,7 +1466,9 @@ namespace {
 int64_t run_batch_impl(int dtype, const void* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
                        const int32_t* dilations, const int32_t* paddings, const void* biases, const void* wflat,
                        const int64_t* woff, const int32_t* chidx, const int64_t* choff, const int32_t* chcnt,
-                       int64_t K, int32_t workers, int32_t fpk, void* out, int64_t ld_out, int64_t row0) {
+                       int64_t K, int32_t workers, int32_t fpk, void* out, int64_t ld_out, int64_t row0,
+                       int32_t mode) {
+  if (mode != RK_MODE_EXACT && mode != RK_MODE_FAST) return -fail(RK_ERR_INVALID, "unknown mode %d", mode);
   if (workers < 1) return -fail(RK_ERR_INVALID, "workers_per_cell must be positive");
   if (K < 1) return -fail(RK_ERR_INVALID, "bank must contain at least one kernel");
   if (!lengths || !dilations || !paddings || !biases || !wflat || !woff || !chidx || !choff || !chcnt)
@@ -1480,13 +1495,14 @@ int64_t run_batch_impl(int dtype, const void* x, int64_t n_inst, int32_t C, int3
   h = fnv(h, wflat, esz * nw);
   h = fnv(h, chidx, 4 * nci);
   key.hash = h;
-  rk_bank_t bank = nullptr;
+  std::shared_ptr<rk_bank_s> bank;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);
     if (it != g_cache.end()) bank = it->second;
   }
   if (!bank) {
+    rk_bank_t created = nullptr;
     int dev = 0;
     cudaGetDevice(&dev);
     std::vector<float> b32, w32;
@@ -1500,24 +1516,19 @@ int64_t run_batch_impl(int dtype, const void* x, int64_t n_inst, int32_t C, int3
       bf = b32.data();
       wf = w32.data();
     }
-    int rc = rk_bank_create(K, C, L, lengths, dilations, paddings, bf, wf, woff, chidx, choff, chcnt, dev, &bank);
+    int rc = rk_bank_create(K, C, L, lengths, dilations, paddings, bf, wf, woff, chidx, choff, chcnt, dev, &created);
     if (rc) return -rc;
+    bank.reset(created, [](rk_bank_s* p) { rk_bank_destroy(p); });
     if (esz == 8) {
-      rc = rk_bank_attach_f64(bank, static_cast<const double*>(biases), static_cast<const double*>(wflat));
-      if (rc) {
-        rk_bank_destroy(bank);
-        return -rc;
-      }
+      rc = rk_bank_attach_f64(bank.get(), static_cast<const double*>(biases), static_cast<const double*>(wflat));
+      if (rc) return -rc;
     }
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    if (g_cache.size() >= 8) {
-      rk_bank_destroy(g_cache.begin()->second);
-      g_cache.erase(g_cache.begin());
-    }
+    if (g_cache.size() >= 8 && !g_cache.count(key)) g_cache.erase(g_cache.begin());
     g_cache[key] = bank;
   }
   int64_t executed = 0;
-  int rc = rk_transform(bank, x, dtype, n_inst, out, ld_out, row0, fpk, RK_MODE_EXACT, nullptr, &executed);
+  int rc = rk_transform(bank.get(), x, dtype, n_inst, out, ld_out, row0, fpk, mode, nullptr, &executed);
   if (rc) return -rc;
   return executed;
 }
@@ -1529,7 +1540,16 @@ int64_t rk_run_batch_f32(const float* x, int64_t n_inst, int32_t C, int32_t L, c
                          const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, float* out,
                          int64_t ld_out, int64_t row0) {
   return run_batch_impl(RK_DTYPE_F32, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
-                        choff, chcnt, K, workers, fpk, out, ld_out, row0);
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0, RK_MODE_EXACT);
+}
+
+int64_t rk_run_batch_f32_mode(const float* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                              const int32_t* dilations, const int32_t* paddings, const float* biases,
+                              const float* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
+                              const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, float* out,
+                              int64_t ld_out, int64_t row0, int32_t mode) {
+  return run_batch_impl(RK_DTYPE_F32, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0, mode);
 }
 
 int64_t rk_run_batch_f64(const double* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
@@ -1538,15 +1558,23 @@ int64_t rk_run_batch_f64(const double* x, int64_t n_inst, int32_t C, int32_t L, 
                          const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, double* out,
                          int64_t ld_out, int64_t row0) {
   return run_batch_impl(RK_DTYPE_F64, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
-                        choff, chcnt, K, workers, fpk, out, ld_out, row0);
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0, RK_MODE_EXACT);
+}
+
+int64_t rk_run_batch_f64_mode(const double* x, int64_t n_inst, int32_t C, int32_t L, const int32_t* lengths,
+                              const int32_t* dilations, const int32_t* paddings, const double* biases,
+                              const double* wflat, const int64_t* woff, const int32_t* chidx, const int64_t* choff,
+                              const int32_t* chcnt, int64_t K, int32_t workers, int32_t fpk, double* out,
+                              int64_t ld_out, int64_t row0, int32_t mode) {
+  return run_batch_impl(RK_DTYPE_F64, x, n_inst, C, L, lengths, dilations, paddings, biases, wflat, woff, chidx,
+                        choff, chcnt, K, workers, fpk, out, ld_out, row0, mode);
 }
 
 int rk_release_caches(void) {
   rk_stream_release();
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    for (auto& kv : g_cache) rk_bank_destroy(kv.second);
-    g_cache.clear();
+    g_cache.clear();  // banks still in use are destroyed by their last user
   }
   std::lock_guard<std::mutex> lk(g_dev_mu);
   for (auto& kv : g_devs) {

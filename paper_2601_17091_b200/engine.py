@@ -242,6 +242,7 @@ class DeviceBank:
         _lib.check(rc, "rk_bank_create")
         self._handle = handle
         self._f64 = False
+        self._f64_lock = threading.Lock()
         info = _lib.BankInfo()
         _lib.check(lib.rk_bank_info(handle, ctypes.byref(info)), "rk_bank_info")
         self.info = {f: getattr(info, f) for f, _ in _lib.BankInfo._fields_}
@@ -251,8 +252,12 @@ class DeviceBank:
         return self._handle
 
     def attach_f64(self):
-        """Upload the float64 bank parameters (precision "double")."""
-        if not self._f64:
+        """Upload the float64 bank parameters (precision "double"); shard
+        threads sharing this bank attach it once, and none transforms before
+        the upload is complete."""
+        with self._f64_lock:
+            if self._f64:
+                return
             bank = self.bank
             self._keep["biases64"] = np.ascontiguousarray(bank.biases, dtype=np.float64)
             self._keep["weights64"] = np.ascontiguousarray(bank.weights, dtype=np.float64)
@@ -302,7 +307,9 @@ def device_bank(bank: KernelBank, device: int = 0) -> DeviceBank:
         db = _bank_cache.get(key)
         if db is None:
             if len(_bank_cache) >= 8:
-                _bank_cache.pop(next(iter(_bank_cache))).close()
+                # dropped, not closed: a thread may still be transforming
+                # with it; __del__ frees it once the last user lets go
+                _bank_cache.pop(next(iter(_bank_cache)))
             db = DeviceBank(bank, device)
             _bank_cache[key] = db
         return db

@@ -21,7 +21,16 @@ import numpy as np
 
 from . import _lib
 from .data import Dataset, cache_layout, load_dataset
-from .engine import CapacityError, GridLimits, TransformStats, _check_request, device_bank, plan_shards
+from .engine import (
+    CapacityError,
+    GridLimits,
+    TransformStats,
+    _check_request,
+    bytes_per_instance,
+    device_bank,
+    plan_batches,
+    plan_shards,
+)
 from .features import FEATURE_DATA_OFFSET, precision_dtype, write_feature_header
 from .kernels import KernelBank
 
@@ -90,6 +99,10 @@ def transform_file(
         in_dtype = values.dtype.type
         in_offset = 0
     _check_dims(n_channels, l_series, bank, limits)
+    # the reference's batch plan raises CapacityError when one series
+    # exceeds the memory budget (engine.py:111-115), before any device work
+    if n:
+        plan_batches(n, bytes_per_instance(n_channels, l_series), limits)
     rk_dtype = _lib.RK_DTYPE_F64 if dtype == np.float64 else _lib.RK_DTYPE_F32
     in_rk = _lib.RK_DTYPE_F64 if in_dtype == np.float64 else _lib.RK_DTYPE_F32
     in_row = n_channels * l_series * np.dtype(in_dtype).itemsize

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_device_count_without_gpu():
     lib = _lib.load()
-    assert lib.rk_abi_version() == 1
+    assert lib.rk_abi_version() == 2
     n = _lib.device_count()
     assert n >= 0
 

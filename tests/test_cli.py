@@ -48,13 +48,24 @@ def test_transform_flags():
 
 
 def test_exit_codes_before_device_work(tmp_path, capsys):
-    # parse error in the dataset -> 2, with the line number
+    # text datasets are out of scope -> ValueError -> 2
     (tmp_path / "bad.ts").write_text("@data\n1,2,x\n")
     assert main(["transform", "--data", str(tmp_path / "bad.ts"), "--kernels", "2", "--out",
                  str(tmp_path / "o")]) == 2
-    assert "line 2" in capsys.readouterr().err
+    assert "not read by this package" in capsys.readouterr().err
     # neither --bank nor --kernels -> 2
     assert main(["transform", "--data", os.path.join(GOLDEN, "two_class.rkds"), "--out", str(tmp_path / "o")]) == 2
     # missing file -> 2 (OSError)
     assert main(["transform", "--data", str(tmp_path / "nope.rkds"), "--kernels", "2", "--out",
                  str(tmp_path / "o")]) == 2
+
+
+def test_capacity_error_exits_3(tmp_path, capsys):
+    """The reference's test_capacity_error_exits_3: a memory budget smaller
+    than one series is a CapacityError (plan_batches, engine.py:111-115),
+    exit code 3, raised before any device work (so it holds without a GPU)."""
+    out = tmp_path / "o.rkfm"
+    assert main(["transform", "--data", os.path.join(GOLDEN, "two_class.rkds"), "--kernels", "4",
+                 "--memory-budget", "16", "--out", str(out)]) == 3
+    assert "capacity error" in capsys.readouterr().err
+    assert not out.exists()

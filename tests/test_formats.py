@@ -1,6 +1,6 @@
 """File formats against files the reference itself wrote
 (tests/golden/formats/, made by tests/golden/make_golden.py:make_formats):
-bank (RKBK), dataset cache (RKDS), feature matrix (RKFM), .ts / .csv text,
+bank (RKBK), dataset cache (RKDS), feature matrix (RKFM) and its CSV export,
 and the reference's own data / feature / bank test cases
 (/root/reference/pkg/tests/test_data.py, test_features.py,
 test_kernels.py:160-195) restated."""
@@ -13,18 +13,13 @@ import pytest
 from paper_2601_17091_b200.binio import FormatError
 from paper_2601_17091_b200.data import (
     Dataset,
-    ParseError,
     cache_layout,
     load_cache,
     load_dataset,
-    parse_csv,
-    parse_ts,
     read_cache_labels,
     save_cache,
     synth_random,
     synth_two_class,
-    write_csv,
-    write_ts,
 )
 from paper_2601_17091_b200.features import FEATURE_DATA_OFFSET, FeatureMatrix
 from paper_2601_17091_b200.kernels import GenOptions, KernelBank, generate_bank
@@ -66,14 +61,6 @@ def test_cache_bytes(tmp_path):
     assert read_bytes(tmp_path / "r.rkds") == read_bytes(golden("random64.rkds"))
 
 
-def test_text_exports_bytes(tmp_path):
-    ds = synth_two_class(3, 40, seed=8)
-    write_ts(ds, tmp_path / "d.ts")
-    write_csv(ds, tmp_path / "d.csv")
-    assert read_bytes(tmp_path / "d.ts") == read_bytes(golden("two_class.ts"))
-    assert read_bytes(tmp_path / "d.csv") == read_bytes(golden("two_class.csv"))
-
-
 @pytest.mark.parametrize("name", ["two_class_single", "two_class_mpv", "two_class_double", "random64_single"])
 def test_feature_file_roundtrip_bytes(tmp_path, name):
     fm = FeatureMatrix.load(golden(name + ".rkfm"))
@@ -106,13 +93,15 @@ def test_cache_layout_and_labels():
     assert read_cache_labels(golden("random64.rkds"), lay64) is None
 
 
-def test_load_dataset_dispatch():
-    a = load_dataset(golden("two_class.ts"))
-    b = load_dataset(golden("two_class.csv"), csv_labels=True)
+def test_load_dataset_dispatch(tmp_path):
     c = load_dataset(golden("two_class.rkds"))
-    assert np.array_equal(a.values, c.values) and np.array_equal(b.values, c.values)
-    assert a.labels == b.labels == c.labels
-    assert a.name == "synth_two_class"
+    assert c.name == "synth_two_class" and c.labels == synth_two_class(3, 40, seed=8).labels
+    np.save(tmp_path / "d.npy", c.values)
+    assert load_dataset(tmp_path / "d.npy").values.tobytes() == c.values.tobytes()
+    # text ingestion is out of scope: a clear error, not a parse
+    for name in ("two_class.ts", "two_class.csv"):
+        with pytest.raises(ValueError, match="not read by this package"):
+            load_dataset(golden(name))
 
 
 def test_truncated_files_raise_format_error(tmp_path):
@@ -144,76 +133,6 @@ def test_bad_magic_and_version(tmp_path):
 
 
 # ---- the reference's data tests (test_data.py) ------------------------------
-
-UNIVARIATE_TS = "@problemName Tiny\n@univariate true\n@equalLength true\n@seriesLength 3\n" \
-                "@classLabel true 0 1\n@data\n1,2,3:0\n"
-MULTIVARIATE_TS = "@problemName Two\n@univariate false\n@dimension 2\n@equalLength true\n" \
-                  "@classLabel true A B\n@data\n1,2:3,4:A\n"
-EMPTY_TS = "@problemName Hollow\n@dimension 2\n@seriesLength 5\n@classLabel false\n@data\n"
-
-
-def test_parse_ts_goldens():
-    ds = parse_ts(UNIVARIATE_TS)
-    assert ds.values[0, 0].tolist() == [1.0, 2.0, 3.0] and ds.labels == ["0"] and ds.name == "Tiny"
-    ds = parse_ts(MULTIVARIATE_TS)
-    assert ds.values.shape == (1, 2, 2) and ds.values[0, 1].tolist() == [3.0, 4.0] and ds.labels == ["A"]
-    ds = parse_ts(EMPTY_TS)
-    assert (ds.n_instances, ds.n_channels, ds.l_series) == (0, 2, 5) and ds.labels is None
-    assert parse_ts(UNIVARIATE_TS.encode()).n_instances == 1
-
-
-@pytest.mark.parametrize(
-    "text,line",
-    [
-        ("@data\n1,2,x\n", 2),
-        ("@classLabel true 0 1\n@data\n1,2:9\n", 3),
-        ("@seriesLength 4\n@data\n1,2,3\n", 3),
-        ("@data\n1,2,3\n1,2\n", 3),
-        ("@dimension 2\n@data\n1,2\n", 3),
-        ("@equalLength false\n@data\n", 1),
-        ("@univariate true\n1,2,3\n@data\n", 2),
-    ],
-)
-def test_parse_ts_error_lines(text, line):
-    with pytest.raises(ParseError) as err:
-        parse_ts(text)
-    assert err.value.line == line
-
-
-def test_parse_ts_other_errors():
-    with pytest.raises(ParseError):
-        parse_ts("@problemName NoData\n")
-    with pytest.raises(ParseError) as err:
-        parse_ts("@classLabel true x y\n@data\n1,2:z\n")
-    assert "unknown class label" in str(err.value)
-
-
-def test_parse_csv_cases():
-    ds = parse_csv("1,2,3\n4,5,6\n")
-    assert ds.values.shape == (2, 1, 3) and ds.labels is None
-    ds = parse_csv("0.5,1.5,A\n", has_labels=True)
-    assert ds.values[0, 0].tolist() == [0.5, 1.5] and ds.labels == ["A"]
-    with pytest.raises(ParseError) as err:
-        parse_csv("1,2,x\n")
-    assert err.value.line == 1
-    with pytest.raises(ParseError) as err:
-        parse_csv("1,2,3\n4,5\n")
-    assert err.value.line == 2
-
-
-def test_ts_roundtrip_random(tmp_path):
-    rng = np.random.Generator(np.random.Philox(key=np.uint64(50)))
-    for trial in range(10):
-        n, c, l = int(rng.integers(0, 6)), int(rng.integers(1, 4)), int(rng.integers(1, 12))
-        values = rng.standard_normal((n, c, l)).astype(np.float32)
-        labels = [str(rng.integers(0, 3)) for _ in range(n)] if trial % 2 else None
-        ds = Dataset(values=values, labels=labels, name=f"T{trial}")
-        write_ts(ds, tmp_path / f"t{trial}.ts")
-        back = load_dataset(tmp_path / f"t{trial}.ts")
-        assert back.values.shape == ds.values.shape and back.labels == ds.labels
-        if n:
-            assert np.array_equal(back.values, ds.values)
-
 
 def test_dataset_invariants():
     with pytest.raises(ValueError):

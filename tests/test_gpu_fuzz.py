@@ -16,7 +16,7 @@ from paper_2601_17091_b200.engine import expected_dot_products
 pytestmark = pytest.mark.gpu
 
 
-def _config(seed, unit_scale=False):
+def _config(seed):
     rng = np.random.Generator(np.random.Philox(key=np.uint64(1000 + seed)))
     l_series = int(rng.choice([11, 12, 13, 17, 31, 64, 97, 100, 255, 256, 513, 1000, 1023, 2049]))
     n_channels = int(rng.choice([1, 1, 1, 2, 3, 5]))
@@ -24,7 +24,7 @@ def _config(seed, unit_scale=False):
     n = int(rng.integers(1, 70))
     center = bool(rng.integers(0, 2))
     scale = float(rng.choice([1e-3, 1.0, 50.0]))
-    values = (rng.standard_normal((n, n_channels, l_series)) * (1.0 if unit_scale else scale)).astype(np.float32)
+    values = (rng.standard_normal((n, n_channels, l_series)) * scale).astype(np.float32)
     if seed % 5 == 0:
         values[:, :, ::7] = 0.0  # exact zeros: ties at the count threshold
     bank = generate_bank(l_series, n_channels, count, GenOptions(seed=seed, center_weights=center))
@@ -43,11 +43,8 @@ def test_fuzz_exact_and_fast(seed, cuda_ready):
     fm, stats = transform_with_stats(values, bank, mode="exact")
     assert fm.values.tobytes() == ref.tobytes()
     assert stats.total_dot_products == expected_dot_products(bank, values.shape[0])
-    # The fast-mode tolerance (MAX within 1e-5 relative) is the north star's
-    # for standard-normal series; at 50x scale the reference's own float32
-    # sums are 2e-5 (relative) from the float64 truth in cancelling cells,
-    # so the fast check runs on unit-scale data of the same shape.
-    values, bank = _config(seed, unit_scale=True)
+    # fast mode on the same (scaled) data: cells float32 cannot resolve to
+    # 1e-5 are certified against float64 (oracle/parity.py), not avoided
     check_fast(transform(values, bank, mode="fast").values, oracle_transform(values, bank), values, bank)
     check_fast(transform(values, bank, mode="fast", include_mpv=True).values,
                oracle_transform(values, bank, include_mpv=True), values, bank, fpk=3)

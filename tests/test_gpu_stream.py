@@ -38,7 +38,6 @@ def read_bytes(path):
         ("two_class.rkds", {}, "two_class_single.rkfm"),
         ("two_class.rkds", {"include_mpv": True}, "two_class_mpv.rkfm"),
         ("two_class.rkds", {"precision": "double"}, "two_class_double.rkfm"),
-        ("two_class.ts", {}, "two_class_single.rkfm"),
         ("random64.rkds", {}, "random64_single.rkfm"),
     ],
 )
@@ -48,12 +47,6 @@ def test_stream_matches_reference_files(cuda_ready, tmp_path, source, kwargs, ex
     assert read_bytes(tmp_path / "f.rkfm") == read_bytes(golden(expect))
     n = FeatureMatrix.load(golden(expect)).n_instances
     assert stats.total_dot_products == engine.expected_dot_products(bank, n)
-
-
-def test_stream_csv_input(cuda_ready, tmp_path):
-    bank = KernelBank.load(golden("bank_40x6.rkbk"))
-    transform_file(golden("two_class.csv"), bank, tmp_path / "f.rkfm", csv_labels=True)
-    assert read_bytes(tmp_path / "f.rkfm") == read_bytes(golden("two_class_single.rkfm"))
 
 
 @pytest.mark.parametrize("batch_rows,devices", [(1, 1), (7, 1), (64, 1), (0, 1), (13, 3)])
@@ -119,7 +112,7 @@ def test_cli_transform_matches_reference_file(cuda_ready, tmp_path):
     assert read_bytes(tmp_path / "f.rkfm") == read_bytes(golden("two_class_single.rkfm"))
     assert read_bytes(tmp_path / "f.csv") == read_bytes(golden("two_class_single.csv"))
     # generated bank (--kernels/--seed) == the saved reference bank
-    r = _cli("transform", "--data", golden("two_class.ts"), "--kernels", "6", "--seed", "5", "--precision",
+    r = _cli("transform", "--data", golden("two_class.rkds"), "--kernels", "6", "--seed", "5", "--precision",
              "double", "--devices", "2", "--out", str(tmp_path / "g.rkfm"))
     assert r.returncode == 0, r.stderr
     assert read_bytes(tmp_path / "g.rkfm") == read_bytes(golden("two_class_double.rkfm"))
@@ -131,6 +124,6 @@ def test_cli_exit_codes(cuda_ready, tmp_path):
     r = _cli("transform", "--data", golden("two_class.rkds"), "--kernels", "6", "--max-x", "3",
              "--out", str(tmp_path / "f.rkfm"))
     assert r.returncode == 3
-    (tmp_path / "bad.ts").write_text("@data\n1,2,x\n")
-    r = _cli("transform", "--data", str(tmp_path / "bad.ts"), "--kernels", "2", "--out", str(tmp_path / "f.rkfm"))
-    assert r.returncode == 2 and "line 2" in r.stderr
+    r = _cli("transform", "--data", golden("two_class.rkds"), "--kernels", "6", "--memory-budget", "16",
+             "--out", str(tmp_path / "f.rkfm"))
+    assert r.returncode == 3 and "capacity error" in r.stderr
