@@ -23,6 +23,11 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .binio import read_array, read_header, read_str, read_values, write_array, write_header, write_str, write_values
+
+MODEL_MAGIC = b"RKRM"
+MODEL_VERSION = 1
+
 
 @dataclass
 class RidgeModel:
@@ -39,6 +44,35 @@ class RidgeModel:
     @property
     def n_features(self) -> int:
         return self.weights.shape[0]
+
+    def save(self, path) -> None:
+        """RKRM v1, the reference's model file (ridge.py:49-67): header,
+        QQdB (n_features, n_outputs, alpha, has_classes), float64 weights,
+        intercepts, means, scales, then the class names."""
+        weights = np.asarray(self.weights, dtype=np.float64)
+        n_features, n_outputs = weights.shape
+        with open(path, "wb") as f:
+            write_header(f, MODEL_MAGIC, MODEL_VERSION)
+            write_values(f, "QQdB", n_features, n_outputs, float(self.alpha), 1 if self.class_names is not None else 0)
+            for arr in (weights, self.intercepts, self.feature_means, self.feature_scales):
+                write_array(f, np.asarray(arr, dtype=np.float64))
+            for name in self.class_names or ():
+                write_str(f, name)
+
+    @classmethod
+    def load(cls, path) -> "RidgeModel":
+        """Read an RKRM v1 file (ridge.py:69-88); FormatError on a bad file."""
+        with open(path, "rb") as f:
+            read_header(f, MODEL_MAGIC, MODEL_VERSION)
+            n_features, n_outputs, alpha, has_classes = read_values(f, "QQdB")
+            nf, no = int(n_features), int(n_outputs)
+            weights = read_array(f, np.float64, nf * no).reshape(nf, no)
+            intercepts = read_array(f, np.float64, no)
+            means = read_array(f, np.float64, nf)
+            scales = read_array(f, np.float64, nf)
+            names = [read_str(f) for _ in range(no)] if has_classes else None
+        return cls(weights=weights, intercepts=intercepts, feature_means=means, feature_scales=scales,
+                   alpha=float(alpha), class_names=names)
 
 
 def _device_of(features, device):

@@ -92,6 +92,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "transforms.npz"), **arrays)
     make_ridge()
     make_formats()
+    make_ridge_models()
 
 
 def make_ridge():
@@ -124,10 +125,10 @@ def make_ridge():
 def make_formats():
     """Files written by the reference's own writers (_binio.py, kernels.py:
     127-147, data.py:193-276, features.py:59-91) for the format parity
-    tests: a bank, dataset caches (f32 with labels, f64 without), .ts and
-    .csv exports, and feature files of reference transforms of the cached
+    tests: a bank, dataset caches (f32 with labels, f64 without), and
+    feature files of reference transforms of the cached
     dataset (single / single+MPV / double) plus one CSV export."""
-    from gridrocket.data import save_cache, write_csv, write_ts
+    from gridrocket.data import save_cache
 
     out = os.path.join(HERE, "formats")
     os.makedirs(out, exist_ok=True)
@@ -137,8 +138,6 @@ def make_formats():
         os.path.join(out, "bank_3ch.rkbk"))
     ds = gr.synth_two_class(3, 40, seed=8)
     save_cache(ds, os.path.join(out, "two_class.rkds"))
-    write_ts(ds, os.path.join(out, "two_class.ts"))
-    write_csv(ds, os.path.join(out, "two_class.csv"))
     ds64 = gr.Dataset(values=gr.synth_random(4, 1, 40, seed=9).values.astype(np.float64) * 1.5,
                       name="random64")
     save_cache(ds64, os.path.join(out, "random64.rkds"))
@@ -150,5 +149,24 @@ def make_formats():
     gr.transform(ds, bank, precision="double").to_csv(os.path.join(out, "two_class_double.csv"))
 
 
+def make_ridge_models():
+    """RKRM v1 model files written by the reference's RidgeModel.save
+    (ridge.py:49-67): a one-vs-rest classifier and a regression model fitted
+    on the reference features of the two-class cache."""
+    from gridrocket import ridge as rr
+    from gridrocket.data import load_cache
+
+    out = os.path.join(HERE, "formats")
+    ds = load_cache(os.path.join(out, "two_class.rkds"))
+    bank = gr.generate_bank(40, 1, 6, gr.GenOptions(seed=5))
+    feats = gr.transform(ds, bank)
+    rr.fit(feats, ds.labels, alpha=0.5).save(os.path.join(out, "ridge_cls.rkrm"))
+    rr.fit_regression(feats, np.arange(ds.values.shape[0], dtype=np.float64), alpha=2.0).save(
+        os.path.join(out, "ridge_reg.rkrm"))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["ridge_models"]:
+        make_ridge_models()
+    else:
+        main()

@@ -133,11 +133,25 @@ def test_pinned_host_pipeline_matches_device_path(mode, cuda_ready):
                                      precision=precision)
         assert executed == expected_dot_products(bank, n)
         assert torch.isnan(out[:3]).all() and torch.isnan(out[:, width:]).all()
-        assert out[3:, :width].contiguous().numpy().tobytes() == ref.numpy().tobytes(), (fpk, precision)
+        _same(out[3:, :width].contiguous().numpy(), ref.numpy(), fpk, mode, precision)
         # the contiguous case bench.py times
         out2 = torch.empty((n, width), dtype=dt).pin_memory()
         db.transform_into(xp.data_ptr(), n, out2.data_ptr(), width, mode=mode, fpk=fpk, precision=precision)
-        assert out2.numpy().tobytes() == ref.numpy().tobytes(), (fpk, precision)
+        _same(out2.numpy(), ref.numpy(), fpk, mode, precision)
+
+
+def _same(got, ref, fpk, mode, precision):
+    """Bytes equal, except fast-mode MPV: its positive sum is reduced in the
+    lane order of the chunk layout, which depends on how many series a call
+    stages per item (a 3,334-row pipeline batch runs the full-warp twin, a
+    20,000-row call the half-warp layout) — PPV and MAX stay bytes-equal,
+    MPV agrees to float32 summation rounding."""
+    if fpk == 3 and mode == "fast" and precision == "single":
+        np.testing.assert_array_equal(got[:, 0::3], ref[:, 0::3])
+        np.testing.assert_array_equal(got[:, 1::3], ref[:, 1::3])
+        np.testing.assert_allclose(got[:, 2::3], ref[:, 2::3], rtol=1e-5, atol=0)  # MPV_RTOL
+    else:
+        assert got.tobytes() == ref.tobytes(), (fpk, precision)
 
 
 @pytest.mark.parametrize("mode", ["fast", "exact"])

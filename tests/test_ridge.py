@@ -89,3 +89,42 @@ def test_transform_to_ridge_on_device(cuda_ready):
     m = ridge.fit(feats[torch.as_tensor(tr, device="cuda")], [labels[i] for i in tr], alpha=best)
     pred = ridge.predict(m, feats[torch.as_tensor(te, device="cuda")])
     assert ridge.accuracy(pred, [labels[i] for i in te]) >= 0.95
+
+
+FORMATS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "formats")
+
+
+@pytest.mark.parametrize("name", ["ridge_cls", "ridge_reg"])
+def test_model_file_roundtrip_matches_reference(name, tmp_path):
+    """RKRM v1 files the reference's RidgeModel.save wrote
+    (tests/golden/make_golden.py:make_ridge_models) load here, re-save byte
+    for byte, and a model fitted here on the same features saves a file the
+    reference layout reads back to the same fit (float64 rounding)."""
+    from paper_2601_17091_b200 import FeatureMatrix, KernelBank
+    from paper_2601_17091_b200.binio import FormatError
+    from paper_2601_17091_b200.data import load_cache
+
+    path = os.path.join(FORMATS, name + ".rkrm")
+    m = ridge.RidgeModel.load(path)
+    m.save(tmp_path / "m.rkrm")
+    assert (tmp_path / "m.rkrm").read_bytes() == open(path, "rb").read()
+    ds = load_cache(os.path.join(FORMATS, "two_class.rkds"))
+    feats = FeatureMatrix.load(os.path.join(FORMATS, "two_class_single.rkfm")).values
+    assert KernelBank.load(os.path.join(FORMATS, "bank_40x6.rkbk")).count * 2 == feats.shape[1]
+    if name == "ridge_cls":
+        assert m.class_names == sorted(set(ds.labels))
+        ours = ridge.fit(feats, ds.labels, alpha=0.5, device="cpu")
+    else:
+        assert m.class_names is None
+        ours = ridge.fit_regression(feats, np.arange(ds.values.shape[0], dtype=np.float64), alpha=2.0, device="cpu")
+    ours.save(tmp_path / "o.rkrm")
+    back = ridge.RidgeModel.load(tmp_path / "o.rkrm")
+    assert back.alpha == m.alpha and back.class_names == m.class_names
+    np.testing.assert_allclose(back.weights, m.weights, rtol=1e-8, atol=1e-11)
+    np.testing.assert_allclose(back.intercepts, m.intercepts, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(back.feature_means, m.feature_means, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(back.feature_scales, m.feature_scales, rtol=1e-12, atol=1e-14)
+    raw = open(path, "rb").read()
+    (tmp_path / "t.rkrm").write_bytes(raw[:-3])
+    with pytest.raises(FormatError):
+        ridge.RidgeModel.load(tmp_path / "t.rkrm")
