@@ -79,7 +79,8 @@ typedef struct rk_bank_info_s {
   int32_t ctas_per_sm;  /* resident CTAs per SM on the wide path */
   int32_t n_half_chunks; /* chunks laid out as half-warp chunks (two series
                             per 16-lane pass) in the fast-mode layout */
-  int32_t reserved;
+  int32_t n_paired_chunks; /* single-kernel chunks run position-paired (the
+                               two FFMA2 lanes on two positions of the kernel) */
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

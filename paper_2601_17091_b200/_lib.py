@@ -74,7 +74,7 @@ class BankInfo(ctypes.Structure):
         ("path", ctypes.c_int32),
         ("ctas_per_sm", ctypes.c_int32),
         ("n_half_chunks", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("n_paired_chunks", ctypes.c_int32),
     ]
 
 

@@ -40,6 +40,17 @@ void fill_half(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   }
 }
 
+// position-paired single-kernel chunks (kinds 6 / 7): PPV/MAX and fast MPV
+template <int RI, int NC>
+void fill_sp(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
+  constexpr int R = rk::r_of(RI);
+  if constexpr (R <= rk::sp_rmax(NC, RK_LEN)) {
+    wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, false, false, false, true>;
+    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, true, false, false, false, true>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, true, false, false, true>;
+  }
+}
+
 // GMEM variants: every chunk uses the run-time slot layout; 2-pair chunks
 // at R <= 5, 1-pair chunks at any R — within registers.
 template <int RI, int P>
@@ -65,6 +76,8 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
   fill_wide<RI, 1, 1>(dt, mt, base + 3);
   fill_half<RI, 2>(dt, mt, base + 4);
   fill_half<RI, 1>(dt, mt, base + 5);
+  fill_sp<RI, 1>(dt, mt, base + 6);
+  fill_sp<RI, 2>(dt, mt, base + 7);
   fill_gmem<RI, 2>(gt, base + 0);
   fill_gmem<RI, 1>(gt, base + 1);
   fill_gmem<RI, 1>(gt, base + 2);

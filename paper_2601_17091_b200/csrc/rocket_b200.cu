@@ -91,6 +91,28 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false
   return nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) * mpct / 100 + 40 * G + chunk_extra;
 }
 
+// Cost of a position-paired single-kernel chunk (kinds 6 / 7): runs of 2R
+// positions per lane, R FFMA2 pairs per tap and slot, two window loads per
+// pair slot.
+int64_t chunk_cost_sp(int len, int d, int n, int nc, int R) {
+  const int64_t RD = 2LL * R * d;
+  const int64_t A = n / RD;
+  const int64_t rem = n - A * RD;
+  const int64_t full_starts = A * d;
+  const int64_t starts = full_starts + std::min<int64_t>(d, rem);
+  const int64_t nfull = full_starts / 32;
+  const int64_t masked_steps = (starts - nfull * 32 + 31) / 32;
+  auto step = [&](int64_t extra) {
+    return (int64_t)R * len * nc      // FFMA2
+           + 2LL * R * 2              // count (2R outputs)
+           + R                        // max (FMNMX3 pairs)
+           + 4LL * (R + len - 1) * nc  // two window loads + addresses per pair slot
+           + extra;
+  };
+  static const int chunk_extra = getenv("RK_CHUNK_COST") ? atoi(getenv("RK_CHUNK_COST")) : 60;
+  return nfull * step(8) + masked_steps * (step(18) + 8LL * R * nc) + 40 * 2 + chunk_extra;
+}
+
 }  // namespace
 
 struct rk_bank_s {
@@ -902,6 +924,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   const int half_ctas = std::min<int>(
       std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))),
       getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6);
+  const bool sp_ok = !getenv("RK_NO_SP");
   const bool half_ok = half_margin > 0 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   std::vector<float> wpack;
@@ -935,6 +958,9 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       const int G = 2 * P;
       const int nk = (int)std::min<size_t>(G, left);
       const int len = lengths[ks[k0]];
+      // a lone kernel runs position-paired (both FFMA2 lanes useful)
+      const bool sp = nk == 1 && nc <= 2 && wide_ok && !gmem && sp_ok;
+      if (sp) nck = nc == 1 ? 6 : 7;
       const int cc = (len - 1) / 2;
       HostChunk hc;
       std::memset(&hc.dev, 0, sizeof(hc.dev));
@@ -952,6 +978,15 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       int64_t best = INT64_MAX;
       bool half = false;
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
+        if (sp) {
+          if (rk::r_of(ri) > rk::sp_rmax(nc, len)) continue;
+          const int64_t cst = chunk_cost_sp(len, d, n, nc, rk::r_of(ri));
+          if (cst < best) {
+            best = cst;
+            best_r = ri;
+          }
+          continue;
+        }
         if (nck == 2 && !wide_ok && ri != 0) continue;  // class-kernel generic path: 1 position per lane
         if (gmem && nck == 0 && ri > 2) continue;  // GMEM slot-loop kernels with 2 pairs: R <= 5 (registers)
         const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), gmem || rk::nck_slots(nck) == 0);
@@ -985,7 +1020,13 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
             for (int h = 0; h < 2; ++h) {
               const int g = 2 * pp + h;
               float w = 0.0f;
-              if (g < nk) {
+              if (sp) {
+                // position-paired: the one kernel's weight in both lanes (w, w)
+                const int64_t k = ks[k0];
+                const int lk = lengths[k], ck = (lk - 1) / 2;
+                const int jj = j - (cc - ck);
+                if (jj >= 0 && jj < lk) w = weights[woff[k] + (int64_t)s * lk + jj];
+              } else if (g < nk) {
                 const int64_t k = ks[k0 + g];
                 const int lk = lengths[k], ck = (lk - 1) / 2;
                 const int jj = j - (cc - ck);
@@ -1254,7 +1295,10 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->device = b->device;
   info->path = b->wide_path ? (b->gmem ? 2 : 1) : 0;
   info->ctas_per_sm = b->wide_ctas_per_sm;
-  for (const auto& hc : b->chunks) info->n_half_chunks += rk::nck_half(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+  for (const auto& hc : b->chunks) {
+    info->n_half_chunks += rk::nck_half(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+    info->n_paired_chunks += rk::nck_sp(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+  }
   if (b->wide_path)
     info->n_launches = (int32_t)b->wide_launches.size();
   else

@@ -62,7 +62,8 @@ constexpr unsigned kFull = 0xffffffffu;
 //   nc_kind 0: 1 channel, 2 kernel pairs; 1: 2 channels, 1 pair;
 //           2: >= 3 channels, 1 pair (wide kernel: channel slots looped at
 //              run time; class kernel: the generic 1-position path);
-//           3: 1 channel, 1 pair; 4 / 5: kinds 0 / 3 as half-warp chunks
+//           3: 1 channel, 1 pair; 4 / 5: kinds 0 / 3 as half-warp chunks;
+//           6 / 7: one kernel over 1 / 2 channels, position-paired
 #ifndef RK_NUM_R
 #define RK_NUM_R 8
 #endif
@@ -78,14 +79,20 @@ __host__ __device__ constexpr int r_of(int r_idx) {
 constexpr int kExactRMax = 13;
 constexpr int kExactRIdx13 = 5;
 static_assert(r_of(kExactRIdx13) == kExactRMax, "R class table");
-constexpr int kNumNck = 6;
+constexpr int kNumNck = 8;
 // (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop.
 // 4 / 5: the 1-channel kinds 0 / 3 run as half-warp chunks (two series per
 // pass); same chunk data, so they fall back to 0 / 3 when items hold one
-// series.
+// series.  6 / 7: single-kernel chunks over 1 / 2 channel slots run
+// position-paired ("SP"): the two FFMA2 lanes hold two positions of the
+// one kernel instead of a kernel and an idle zero-weight slot.
 __host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4) ? 2 : 1; }
-__host__ __device__ constexpr int nck_slots(int nck) { return nck == 1 ? 2 : nck == 2 ? 0 : 1; }
-__host__ __device__ constexpr bool nck_half(int nck) { return nck >= 4; }
+__host__ __device__ constexpr int nck_slots(int nck) { return (nck == 1 || nck == 7) ? 2 : nck == 2 ? 0 : 1; }
+__host__ __device__ constexpr bool nck_half(int nck) { return nck == 4 || nck == 5; }
+__host__ __device__ constexpr bool nck_sp(int nck) { return nck >= 6; }
+// largest R of the position-paired kinds (2R positions per lane: the pair
+// window and accumulators fit the ~80-register budget)
+__host__ __device__ constexpr int sp_rmax(int nc, int len) { return nc == 1 ? (len == 7 ? 9 : 7) : 5; }
 __host__ __device__ constexpr int nck_full(int nck) { return nck == 4 ? 0 : nck == 5 ? 3 : nck; }
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
@@ -449,6 +456,127 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
       s -= d;
       v0 += RD - d;
     }
+  }
+}
+
+// Position-paired step (single-kernel chunks, kinds 6 / 7): a lane's run
+// holds 2R positions u0 + m*d (m < 2R); FFMA2 lane .x computes position r,
+// lane .y position r + R, both with the one kernel's weight (w, w) and the
+// series values (x[r + j], x[r + R + j]) — a kernel slot that would idle
+// beside a zero-weight partner does useful work instead.  Window element e
+// is loaded into pair slot e (.x) and pair slot e - R (.y); the masking
+// follows load_window_masked element by element (a dead position's last
+// tap reads the canonical NaN).  Per output the arithmetic is the one of
+// chunk_step: same taps, same order, same rounding.
+template <int LEN, int R>
+__device__ __forceinline__ float sp_load(const float* p, int e, int d, int nleft, const float* nan_slot, bool masked) {
+  const float* a = p + e * d;
+  if (masked && e >= LEN - 1) a = (e - (LEN - 1)) * d < nleft ? a : nan_slot;
+  return *a;
+}
+
+template <int LEN, int R, int NC, bool EXACT, bool MASKED, bool MPV = false>
+__device__ __forceinline__ void chunk_step_sp(Pool<2, MPV>& st, const float* const (&chan)[NC],
+                                              const float (&w)[NC][LEN], const float (&thr)[2], float2 init,
+                                              float2 one2, int u0, int d, int nleft, const float* nan_slot) {
+  constexpr int C = (LEN - 1) / 2;
+  constexpr int W = R + LEN - 1;
+  float2 acc[1][R];
+#pragma unroll
+  for (int s = 0; s < NC; ++s) {
+    const float* p = chan[s] + (u0 - C * d);
+    float2 xp[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      xp[q].x = sp_load<LEN, R>(p, q, d, nleft, nan_slot, MASKED);
+      xp[q].y = sp_load<LEN, R>(p, q + R, d, nleft, nan_slot, MASKED);
+    }
+#pragma unroll
+    for (int j = 0; j < LEN; ++j) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        // the weight as a broadcast scalar (one uniform register)
+        const float2 w2 = make_float2(w[s][j], w[s][j]);
+        if (EXACT) {
+          if (s == 0 && j == 0)
+            acc[0][r] = fmul2(xp[r + j], w2);  // RN(w*x) == RN(+0 + RN(w*x))
+          else
+            acc[0][r] = ffma2(fmul2(xp[r + j], w2), one2, acc[0][r]);
+        } else {
+          acc[0][r] = ffma2(xp[r + j], w2, (s == 0 && j == 0) ? init : acc[0][r]);
+        }
+      }
+    }
+  }
+  // slot 0 pools positions r, slot 1 positions r + R (same kernel)
+  pool_update<R, 1, EXACT, false, MPV>(st, acc, thr, true, 0, d);
+}
+
+// run_positions for position-paired chunks: the lane map of run_positions
+// with runs of 2R positions.
+template <int LEN, int R, int NC, bool EXACT, bool MPV = false>
+__device__ __forceinline__ void run_positions_sp(Pool<2, MPV>& st, const float* const (&chan)[NC],
+                                                 const float (&w)[NC][LEN], const float (&thr)[2], float2 init,
+                                                 float2 one2, int lo, int n, int d, int q32, int r32, float invd,
+                                                 const float* nan_slot, int lane) {
+  const int RD = 2 * R * d;
+  const int A = n / RD;
+  const int rem = n - A * RD;
+  const int full_starts = A * d;
+  const int starts = full_starts + min(d, rem);
+  const int nfull = full_starts >> 5;
+  int a = (int)((lane + 0.5f) * invd);
+  int s = lane - a * d;
+  int v0 = a * RD + s;
+  const int dv = q32 * RD + r32;
+#pragma unroll(kStepUnroll)
+  for (int stp = 0; stp < nfull; ++stp) {
+    chunk_step_sp<LEN, R, NC, EXACT, false, MPV>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
+    }
+  }
+  for (int base = nfull << 5; base < starts; base += 32) {
+    const bool live = base + lane < starts;
+    chunk_step_sp<LEN, R, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
+                                                live ? n - v0 : 0, nan_slot);
+    s += r32;
+    v0 += dv;
+    if (s >= d) {
+      s -= d;
+      v0 += RD - d;
+    }
+  }
+}
+
+// Finish a position-paired chunk: merge the two position slots (the
+// CellAccumulator merge, engine.py:58-96), reduce over the warp, lane 0
+// writes the kernel's features.
+template <bool EXACT, class CH, bool MPV = false>
+__device__ __forceinline__ void finish_chunk_sp(const CH& c, Pool<2, MPV>& st, float* __restrict__ orow, int fpk,
+                                                int vec_out, int lane) {
+  const unsigned tot = __reduce_add_sync(kFull, st.cnt[0] + st.cnt[1]);
+  const float e = EXACT ? warp_max(fmaxf(st.ext[0], st.ext[1])) : warp_min(fminf(st.ext[0], st.ext[1]));
+  float ps = 0.0f;
+  if (MPV) {
+    ps = st.ps[0].x + st.ps[0].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(kFull, ps, o);
+  }
+  if (lane == 0) {
+    const float ppv = __fdiv_rn((float)tot, (float)c.n);  // == f32(RN64(count / l_out)), see finish_chunk
+    const float mx = EXACT ? __fadd_rn(e, c.bias[0]) : -e;
+    float* dst = orow + (int64_t)c.col[0] * fpk;
+    if (vec_out) {
+      *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
+    } else {
+      dst[0] = ppv;
+      dst[1] = mx;
+    }
+    if (MPV) dst[2] = tot ? __double2float_rn((double)(-ps) / (double)tot) : 0.0f;  // see finish_chunk
   }
 }
 
@@ -1039,7 +1167,8 @@ __device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned 
                : "memory");
 }
 
-template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false, bool HALF = false>
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false, bool HALF = false,
+          bool SP = false>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_item;
@@ -1128,6 +1257,31 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         }
       } else {
         const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
+        if constexpr (SP) {
+          // position-paired single-kernel chunk: the host packed (w, w)
+          static_assert(P == 1 && !HALF && !GMEM, "position-paired chunks: one kernel, full warp, staged series");
+          float ws[NC][LEN];
+#pragma unroll
+          for (int s = 0; s < NC; ++s)
+#pragma unroll
+            for (int j = 0; j < LEN; ++j) ws[s][j] = wp[s * LEN + j].x;
+          const float thr2[2] = {thr[0], thr[0]};
+          const float2 init2 = make_float2(init[0].x, init[0].x);
+          for (int si = 0; si < ns; ++si) {
+            const float* sx = sbase + si * slot + H;
+            const float* chan[NC];
+#pragma unroll
+            for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
+            Pool<2, MPV> st;
+            pool_init<2, EXACT, MPV>(st);
+            run_positions_sp<LEN, R, NC, EXACT, MPV>(st, chan, ws, thr2, init2, one2, c.lo, c.n, c.d, c.q32, c.r32,
+                                                     c.invd, nanp, lane);
+            finish_chunk_sp<EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out,
+                                                lane);
+            done += (unsigned long long)c.n;
+          }
+          continue;
+        }
         float2 w[NC][P][LEN];
 #pragma unroll
         for (int s = 0; s < NC; ++s)

@@ -354,3 +354,36 @@ def test_half_warp_chunks_exact(n, cuda_ready):
     check_fast(transform(values, bank, mode="fast").values, ref, values, bank)
     ref3 = oracle_transform(values, bank, include_mpv=True)
     check_fast(transform(values, bank, include_mpv=True, mode="fast").values, ref3, values, bank, fpk=3)
+
+
+@pytest.mark.parametrize("channels", [1, 3])
+def test_position_paired_chunks(channels, cuda_ready, monkeypatch):
+    """Lone kernels (a group of one) run position-paired: the two FFMA2 lanes
+    hold two positions of the one kernel (kinds 6 / 7, 1 or 2 channel
+    slots).  Exact mode stays byte-identical to the oracle and to the layout
+    without pairing (RK_NO_SP); fast mode (with MPV) within tolerance."""
+    from oracle.oracle import oracle_transform
+
+    bank = generate_bank(2048, channels, 400, GenOptions(seed=91))
+    db = device_bank(bank, 0)
+    assert db.info["n_paired_chunks"] > 0
+    values = synth_random(700, channels, 2048, seed=92).values
+    ref = oracle_transform(values[:40], bank)
+    exact = transform(values, bank, mode="exact").values
+    assert exact[:40].tobytes() == ref.tobytes()
+    check_fast(transform(values[:40], bank, mode="fast").values, ref, values[:40], bank)
+    ref3 = oracle_transform(values[:40], bank, include_mpv=True)
+    check_fast(transform(values[:40], bank, mode="fast", include_mpv=True).values, ref3, values[:40], bank, fpk=3)
+    monkeypatch.setenv("RK_NO_SP", "1")
+    from paper_2601_17091_b200.engine import DeviceBank
+
+    plain = DeviceBank(bank, 0)
+    assert plain.info["n_paired_chunks"] == 0
+    import torch
+
+    x = torch.from_numpy(values).cuda()
+    out = torch.empty((values.shape[0], bank.count * 2), device="cuda")
+    plain.transform_into(x.data_ptr(), values.shape[0], out.data_ptr(), out.shape[1], mode="exact")
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == exact.tobytes()
+    plain.close()
