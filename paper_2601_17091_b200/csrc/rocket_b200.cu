@@ -565,20 +565,44 @@ int launch_cellrow(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStre
   return RK_OK;
 }
 
+// Position-paired cell kernel: two staged copies of the series (copy 1
+// shifted by one element) so every (x[e], x[e+1]) pair is one aligned load.
+template <typename T, bool MPV, int LEN>
+int launch_cellpair(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStream_t stream) {
+  auto fn = rk::rocket_cellpair_kernel<T, MPV, LEN>;
+  int rc = set_kernel_smem(st, (const void*)fn, (int)smem);
+  if (rc) return rc;
+  int per_sm = 1;
+  RK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+  const int64_t grid = std::min<int64_t>(a.n_series, (int64_t)st->sms * std::max(1, per_sm));
+  fn<<<(unsigned)grid, 256, smem, stream>>>(a);
+  RK_CUDA(cudaGetLastError());
+  return RK_OK;
+}
+
 template <typename T, bool MPV, bool GMEM>
 int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t stream, int* d_counters) {
   const size_t smem = GMEM ? 0 : (size_t)b->C * b->sstride * sizeof(T);
+  // the paired kernel when its two copies leave room for two CTAs per SM
+  const bool paired = !GMEM && !getenv("RK_NO_CELLPAIR") && 2 * (2 * smem + 1024) <= st->smem_optin + 1024;
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * 3, stream));
   a.halo = b->halo;
   a.sstride = b->sstride;
+  a.one = 1.0f;
   for (int li = 0; li < 3; ++li) {
     if (b->cell_len_end[li] <= b->cell_len_begin[li]) continue;
     a.k_begin = (int)b->cell_len_begin[li];
     a.k_end = (int)b->cell_len_end[li];
     a.item_counter = d_counters + li;
-    const int rc = li == 0 ? launch_cellrow<T, MPV, 7, GMEM>(st, a, smem, stream)
-                 : li == 1 ? launch_cellrow<T, MPV, 9, GMEM>(st, a, smem, stream)
-                           : launch_cellrow<T, MPV, 11, GMEM>(st, a, smem, stream);
+    int rc;
+    if (paired)
+      rc = li == 0 ? launch_cellpair<T, MPV, 7>(st, a, 2 * smem, stream)
+         : li == 1 ? launch_cellpair<T, MPV, 9>(st, a, 2 * smem, stream)
+                   : launch_cellpair<T, MPV, 11>(st, a, 2 * smem, stream);
+    else
+      rc = li == 0 ? launch_cellrow<T, MPV, 7, GMEM>(st, a, smem, stream)
+         : li == 1 ? launch_cellrow<T, MPV, 9, GMEM>(st, a, smem, stream)
+                   : launch_cellrow<T, MPV, 11, GMEM>(st, a, smem, stream);
     if (rc) return rc;
   }
   return RK_OK;
@@ -1051,6 +1075,19 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       }
       b->chunks.push_back(hc);
       k0 += nk;
+    }
+  }
+  // RK_DUMP_CHUNKS=<path>: the chunk layout, one line per chunk (diagnostics)
+  if (const char* dump = getenv("RK_DUMP_CHUNKS")) {
+    if (FILE* f = fopen(dump, "a")) {
+      fprintf(f, "# bank K=%lld C=%d L=%d half_margin=%lld\n", (long long)K, C, L, (long long)half_margin);
+      for (const auto& hc : b->chunks) {
+        const rk::DevChunk& c = hc.dev;
+        fprintf(f, "len=%d R=%d nck=%d d=%d lo=%d n=%d nk=%d nc=%d cost=%lld\n", c.len,
+                rk::r_of((c.cls / rk::kNumNck) % rk::kNumR), c.cls % rk::kNumNck, c.d, c.lo, c.n, c.nk, c.nc,
+                (long long)hc.cost);
+      }
+      fclose(f);
     }
   }
   // Both modes accumulate the taps without the bias and count acc > -bias

@@ -927,6 +927,7 @@ struct CellArgs {
   int halo;              // zero halo per side of a staged row (elements)
   int sstride;           // elements per staged channel row
   const void* xpad;      // GMEM: zero-haloed rows of this launch's series
+  float one;             // 1.0f, opaque to ptxas (FMUL2 + FFMA2 stay unfused)
 };
 
 template <typename T>
@@ -1104,6 +1105,163 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
               T v = acc[0];
 #pragma unroll
               for (int r = 1; r < B; ++r) v = q == r ? acc[r] : v;
+              pool(v);
+            }
+          }
+        }
+      }
+      if (live) {
+        T* o = reinterpret_cast<T*>(a.out) + i * a.ld_out + (int64_t)kd.col * a.fpk;
+        o[0] = from_double<T>((double)count / (double)kd.l_out);
+        o[1] = mx;
+        if (MPV) o[2] = count > 0 ? from_double<T>((double)psum / (double)count) : T(0);
+        done += (unsigned long long)kd.l_out;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) done += __shfl_xor_sync(kFull, done, o);
+  if (lane == 0 && done) atomicAdd(a.executed, done);
+}
+
+// Position-paired cell kernel (precision "double" and exact MPV when two
+// staged copies of a series fit): the reference's loop (engine.py:157-188,
+// 202-247) with lane = kernel as in rocket_cellrow_kernel, but positions
+// are evaluated in pairs (t, t + 1), t even: float32 taps as one FMUL2 and
+// one FFMA2(prod, 1, acc) per pair — RN(acc + RN(w*x)) for each position,
+// the same roundings in the same order — and the pair of series values
+// (x[e], x[e + 1]) read with one 8-byte (16-byte for double) shared load.
+// The series is staged twice, copy 1 shifted by one element, so that every
+// pair is aligned in one of the copies: element e even -> copy 0 at e, e odd
+// -> copy 1 at e - 1.  Per lane the copy depends only on the parity of
+// (row offset + j*d), so two base pointers per channel slot (even and odd
+// taps) replace any per-load selection.  MPV sums the positive outputs in
+// position order (t, then t + 1), as the reference does.
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> {
+  using V = float2;
+};
+template <>
+struct Pair<double> {
+  using V = double2;
+};
+
+template <typename T>
+__device__ __forceinline__ typename Pair<T>::V pair_tap(typename Pair<T>::V acc, T w, typename Pair<T>::V x,
+                                                       float2 one2, bool first);
+template <>
+__device__ __forceinline__ float2 pair_tap<float>(float2 acc, float w, float2 x, float2 one2, bool) {
+  return ffma2(fmul2(x, make_float2(w, w)), one2, acc);  // RN(RN(w*x) * 1 + acc) == RN(acc + RN(w*x))
+}
+template <>
+__device__ __forceinline__ double2 pair_tap<double>(double2 acc, double w, double2 x, float2, bool) {
+  return make_double2(__dadd_rn(acc.x, __dmul_rn(w, x.x)), __dadd_rn(acc.y, __dmul_rn(w, x.y)));
+}
+
+template <typename T, bool MPV, int LEN>
+__global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) {
+  using V = typename Pair<T>::V;
+  extern __shared__ __align__(16) unsigned char cell_smem[];
+  T* copy0 = reinterpret_cast<T*>(cell_smem);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
+  T* copy1 = copy0 + C * S;
+  __shared__ int s_item, s_next;
+  for (int k = tid; k < 2 * C * S; k += blockDim.x) copy0[k] = T(0);
+  const int ngroups = (a.k_end - a.k_begin + 31) / 32;
+  const T* wts = reinterpret_cast<const T*>(a.weights);
+  const T* bis = reinterpret_cast<const T*>(a.biases);
+  const float2 one2 = make_float2(a.one, a.one);
+  unsigned long long done = 0;
+  while (true) {
+    __syncthreads();  // every warp has left the previous series (and the zeroing is done)
+    if (tid == 0) {
+      s_item = atomicAdd(a.item_counter, 1);
+      s_next = 0;
+    }
+    __syncthreads();
+    const int64_t i = s_item;
+    if (i >= a.n_series) break;
+    const T* xi = reinterpret_cast<const T*>(a.x) + i * (int64_t)C * L;
+    for (int k = tid; k < C * L; k += blockDim.x) {
+      const int c = k / L, t = k - c * L;
+      const T v = xi[k];
+      copy0[c * S + H + t] = v;
+      copy1[c * S + H + t - 1] = v;
+    }
+    __syncthreads();
+    while (true) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(&s_next, 1);
+      g = __shfl_sync(kFull, g, 0);
+      if (g >= ngroups) break;
+      const int ks = a.k_begin + g * 32 + lane;
+      const bool live = ks < a.k_end;
+      const CellKernel kd = a.kernels[live ? ks : a.k_begin + g * 32];
+      const int lout = live ? kd.l_out : 0;
+      const int span = __reduce_max_sync(kFull, lout);
+      const T bias = bis[live ? ks : a.k_begin + g * 32];
+      const T* wk = wts + kd.woff;
+      const int d = kd.d;
+      T w0[LEN];  // slot-0 weights, kept for the whole walk
+#pragma unroll
+      for (int j = 0; j < LEN; ++j) w0[j] = wk[j];
+      // even taps start at parity(off), odd taps at parity(off + d)
+      const int off0 = __ldg(a.chidx + kd.choff) * S + H - kd.p;
+      const T* q00 = (off0 & 1) ? copy1 + off0 - 1 : copy0 + off0;
+      const T* q01 = ((off0 + d) & 1) ? copy1 + off0 - 1 : copy0 + off0;
+      int count = 0;
+      T mx = T(-INFINITY), psum = T(0);
+      for (int t0 = 0; t0 < span; t0 += 4) {
+        // dead positions (t >= l_out) re-read the last live block; its
+        // start is kept even (pairs (t, t + 1) stay aligned) and reads at
+        // most one position past l_out (inside the row's zero slack)
+        int tb = min(t0, max(lout - 4, 0));
+        tb += tb & 1;
+        V acc0, acc1;  // acc = +0, then RN(acc + RN(w*x)) tap by tap (engine.py:172-179)
+        acc0.x = acc0.y = acc1.x = acc1.y = T(0);
+#pragma unroll
+        for (int j = 0; j < LEN; ++j) {
+          const T* xp = ((j & 1) ? q01 : q00) + j * d + tb;
+          acc0 = pair_tap<T>(acc0, w0[j], *reinterpret_cast<const V*>(xp), one2, false);
+          acc1 = pair_tap<T>(acc1, w0[j], *reinterpret_cast<const V*>(xp + 2), one2, false);
+        }
+        for (int c = 1; c < kd.nc; ++c) {
+          const int off = __ldg(a.chidx + kd.choff + c) * S + H - kd.p;
+          const T* q0 = (off & 1) ? copy1 + off - 1 : copy0 + off;
+          const T* q1 = ((off + d) & 1) ? copy1 + off - 1 : copy0 + off;
+          const T* wc = wk + c * LEN;
+#pragma unroll
+          for (int j = 0; j < LEN; ++j) {
+            const T* xp = ((j & 1) ? q1 : q0) + j * d + tb;
+            const T wj = wc[j];
+            acc0 = pair_tap<T>(acc0, wj, *reinterpret_cast<const V*>(xp), one2, false);
+            acc1 = pair_tap<T>(acc1, wj, *reinterpret_cast<const V*>(xp + 2), one2, false);
+          }
+        }
+        auto pool = [&](T v) {
+          // branch-free: the count and the ordered positive sum advance
+          // only on positive outputs (the sum's order is the position order)
+          v = add_rn<T>(v, bias);
+          const bool pos = v > T(0);
+          count += pos ? 1 : 0;
+          if (MPV) psum = pos ? add_rn<T>(psum, v) : psum;
+          mx = v > mx ? v : mx;
+        };
+        const int shift = t0 - tb;
+        if (shift == 0 && t0 + 4 <= lout) {
+          pool(acc0.x);
+          pool(acc0.y);
+          pool(acc1.x);
+          pool(acc1.y);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int q = b + shift;
+            if (t0 + b < lout) {
+              const T v = q == 0 ? acc0.x : q == 1 ? acc0.y : q == 2 ? acc1.x : acc1.y;
               pool(v);
             }
           }
