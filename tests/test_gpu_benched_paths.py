@@ -18,6 +18,8 @@
 Reference: /root/reference/pkg/src/gridrocket/engine.py:148-190 (the
 per-cell loop), SPEC.md:450-459 (acceptance criteria)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -137,6 +139,14 @@ def test_pinned_host_pipeline_matches_device_path(mode, cuda_ready):
         # the contiguous case bench.py times
         out2 = torch.empty((n, width), dtype=dt).pin_memory()
         db.transform_into(xp.data_ptr(), n, out2.data_ptr(), width, mode=mode, fpk=fpk, precision=precision)
+        _same(out2.numpy(), ref.numpy(), fpk, mode, precision)
+        # a geometric batch schedule (small tail batches: 700, 1400, 2800, ...)
+        os.environ["RK_E2E_TAIL"] = "700"
+        try:
+            out2.zero_()
+            db.transform_into(xp.data_ptr(), n, out2.data_ptr(), width, mode=mode, fpk=fpk, precision=precision)
+        finally:
+            del os.environ["RK_E2E_TAIL"]
         _same(out2.numpy(), ref.numpy(), fpk, mode, precision)
 
 
