@@ -12,6 +12,9 @@ import sys
 _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("RK_LIB_PATH") or os.path.join(_PKG, "_build", "librocket_b200.so")
+# the checked build (-DRK_CHECKED: device-side bounds checks that trap on a
+# bad shared/global access; compute-sanitizer is closed on the GPU pool)
+CHECKED_LIB_PATH = os.path.join(_PKG, "_build", "librocket_b200_checked.so")
 CSRC = os.path.join(_PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 

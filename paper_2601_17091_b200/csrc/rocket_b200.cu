@@ -910,8 +910,20 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   if (rc) return rc;
 
   // Staged series: C channels of [halo zeros | L values | halo zeros],
-  // stride rounded to 32 floats + 1 bank offset between channels.
-  const int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + 4;
+  // stride rounded to 32 floats plus a pad e (a multiple of 4 floats: rows
+  // stay 16-byte aligned for the bulk copies) chosen so that consecutive
+  // staged series sit 16 banks apart (C * e = 16 mod 32): a half-warp
+  // chunk's lanes 0-15 (series A) and 16-31 (series B) then read disjoint
+  // bank halves instead of overlapping ones (r01: 55 % of the shared-load
+  // wavefronts were bank-conflict replays at e = 4).
+  int spad = 4;
+  for (int e = 4; e < 32; e += 4)
+    if ((C * e) % 32 == 16) {
+      spad = e;
+      break;
+    }
+  if (getenv("RK_SSTRIDE_PAD")) spad = std::max(4, atoi(getenv("RK_SSTRIDE_PAD")) / 4 * 4);
+  const int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + spad;
   const int64_t smem = (int64_t)C * sstride * 4;
   // A series that does not fit in shared memory is read from zero-haloed
   // rows in global memory instead (L1 / L2 resident; the wide kernel's

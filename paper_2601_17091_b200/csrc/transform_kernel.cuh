@@ -140,6 +140,61 @@ struct LaunchArgs {
   float one;               // 1.0f, opaque to ptxas (keeps FMUL2 + FFMA2 unfused)
 };
 
+// ---- checked build (-DRK_CHECKED): device-side bounds checks ------------
+// compute-sanitizer is closed on the GPU pool, so the library carries its
+// own memory checks: every window read must fall inside the CTA's dynamic
+// shared memory (or the canonical NaN slot), or — for series read from
+// global memory — inside the zero-haloed row scratch; every feature store
+// inside rows [0, n_series) of the launch's output; __trap() otherwise.
+// Without RK_CHECKED the macros are empty and the kernels are unchanged.
+#ifdef RK_CHECKED
+__shared__ unsigned rk_chk_s_lo, rk_chk_s_hi;          // dynamic smem [lo, hi)
+__shared__ const void* rk_chk_nan;                     // the canonical NaN slot
+__shared__ const char *rk_chk_g_lo, *rk_chk_g_hi;      // global series rows
+__shared__ const char *rk_chk_o_lo, *rk_chk_o_hi;      // output rows
+__device__ __forceinline__ unsigned rk_dyn_smem_bytes() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ void rk_chk_set(const void* smem_base, const void* nan, const void* g_lo,
+                                           const void* g_hi, const void* o_lo, const void* o_hi) {
+  rk_chk_s_lo = static_cast<unsigned>(__cvta_generic_to_shared(smem_base));
+  rk_chk_s_hi = rk_chk_s_lo + rk_dyn_smem_bytes();
+  rk_chk_nan = nan;
+  rk_chk_g_lo = static_cast<const char*>(g_lo);
+  rk_chk_g_hi = static_cast<const char*>(g_hi);
+  rk_chk_o_lo = static_cast<const char*>(o_lo);
+  rk_chk_o_hi = static_cast<const char*>(o_hi);
+}
+__device__ __forceinline__ void rk_chk_read(const void* a, int bytes) {
+  if (a == rk_chk_nan) return;
+  if (__isShared(a)) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(a));
+    if (s < rk_chk_s_lo || s + bytes > rk_chk_s_hi) __trap();
+  } else {
+    const char* c = static_cast<const char*>(a);
+    if (c < rk_chk_g_lo || c + bytes > rk_chk_g_hi) __trap();
+  }
+}
+__device__ __forceinline__ void rk_chk_write(const void* a, int bytes) {
+  const char* c = static_cast<const char*>(a);
+  if (c < rk_chk_o_lo || c + bytes > rk_chk_o_hi) __trap();
+}
+#define RK_CHK_READ(a, bytes) ::rk::rk_chk_read((a), (bytes))
+#define RK_CHK_WRITE(a, bytes) ::rk::rk_chk_write((a), (bytes))
+#define RK_CHK_SET(...) ::rk::rk_chk_set(__VA_ARGS__)
+#define RK_CHK(cond) \
+  do {               \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define RK_CHK_READ(a, bytes) ((void)0)
+#define RK_CHK_WRITE(a, bytes) ((void)0)
+#define RK_CHK_SET(...) ((void)0)
+#define RK_CHK(cond) ((void)0)
+#endif
+
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
@@ -185,7 +240,10 @@ __device__ __forceinline__ void load_window(float (&xw)[R + LEN - 1], const floa
   constexpr int C = (LEN - 1) / 2;
   const float* p = chan + (u0 - C * d);
 #pragma unroll
-  for (int q = 0; q < R + LEN - 1; ++q) xw[q] = p[q * d];
+  for (int q = 0; q < R + LEN - 1; ++q) {
+    RK_CHK_READ(p + q * d, 4);
+    xw[q] = p[q * d];
+  }
 }
 
 // Masked steps: a lane's valid positions are a prefix r < rcount of its
@@ -206,6 +264,7 @@ __device__ __forceinline__ void load_window_masked(float (&xw)[R + LEN - 1], con
   for (int q = 0; q < R + LEN - 1; ++q) {
     const float* a = p + q * d;
     if (q >= LEN - 1) a = (q - (LEN - 1)) * d < nleft ? a : nan_slot;
+    RK_CHK_READ(a, 4);
     xw[q] = *a;
   }
 }
@@ -322,6 +381,7 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G, MPV>& st, floa
     // exact: RN(max_t acc_t + b) == max_t RN(acc_t + b); fast: -min acc'
     const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
     float* dst = orow + (int64_t)my_col * fpk;
+    RK_CHK_WRITE(dst, (MPV ? 3 : 2) * 4);
     if (vec_out) {
       *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
     } else {
@@ -370,6 +430,7 @@ __device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G, MPV>& st,
     const float ppv = __fdiv_rn((float)my_cnt, (float)c.n);  // == f32(RN64(count / l_out)), see finish_chunk
     const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
     float* dst = orow + (int64_t)my_col * fpk;
+    RK_CHK_WRITE(dst, (MPV ? 3 : 2) * 4);
     if (vec_out) {
       *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
     } else {
@@ -472,6 +533,7 @@ template <int LEN, int R>
 __device__ __forceinline__ float sp_load(const float* p, int e, int d, int nleft, const float* nan_slot, bool masked) {
   const float* a = p + e * d;
   if (masked && e >= LEN - 1) a = (e - (LEN - 1)) * d < nleft ? a : nan_slot;
+  RK_CHK_READ(a, 4);
   return *a;
 }
 
@@ -570,6 +632,7 @@ __device__ __forceinline__ void finish_chunk_sp(const CH& c, Pool<2, MPV>& st, f
     const float ppv = __fdiv_rn((float)tot, (float)c.n);  // == f32(RN64(count / l_out)), see finish_chunk
     const float mx = EXACT ? __fadd_rn(e, c.bias[0]) : -e;
     float* dst = orow + (int64_t)c.col[0] * fpk;
+    RK_CHK_WRITE(dst, (MPV ? 3 : 2) * 4);
     if (vec_out) {
       *reinterpret_cast<float2*>(dst) = make_float2(ppv, mx);
     } else {
@@ -785,7 +848,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rocket_class_kernel(cons
   __shared__ float s_nan;  // the masked steps' dead-position source
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  if (tid == 0) s_nan = __int_as_float(0x7fffffff);
+  if (tid == 0) {
+    s_nan = __int_as_float(0x7fffffff);
+    RK_CHK_SET(smem, &s_nan, nullptr, nullptr, a.out, a.out + a.n_series * a.ld_out);
+  }
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
   const int SPI = a.series_per_item;
   const int slot_floats = C * S;
@@ -1012,6 +1078,10 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
   __shared__ int s_item, s_next;
   const int tid = threadIdx.x, lane = tid & 31;
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
+  if (tid == 0)
+    RK_CHK_SET(xstage, nullptr, a.xpad,
+               GMEM ? reinterpret_cast<const T*>(a.xpad) + a.n_series * (int64_t)C * S : nullptr,
+               a.out, reinterpret_cast<T*>(a.out) + a.n_series * a.ld_out);
   if constexpr (!GMEM) {
     for (int k = tid; k < C * S; k += blockDim.x) {
       const int t = k % S;
@@ -1069,6 +1139,7 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 #pragma unroll
         for (int j = 0; j < LEN; ++j) {
           const T* xp = x0 + tb + j * kd.d;
+          RK_CHK_READ(xp, B * (int)sizeof(T));
 #pragma unroll
           for (int b = 0; b < B; ++b) acc[b] = add_rn<T>(acc[b], mul_rn<T>(w0[j], xp[b]));
         }
@@ -1078,6 +1149,7 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 #pragma unroll
           for (int j = 0; j < LEN; ++j) {
             const T wj = wc[j];
+            RK_CHK_READ(xc + j * kd.d, B * (int)sizeof(T));
 #pragma unroll
             for (int b = 0; b < B; ++b) acc[b] = add_rn<T>(acc[b], mul_rn<T>(wj, xc[j * kd.d + b]));
           }
@@ -1112,6 +1184,7 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
       }
       if (live) {
         T* o = reinterpret_cast<T*>(a.out) + i * a.ld_out + (int64_t)kd.col * a.fpk;
+        RK_CHK_WRITE(o, (MPV ? 3 : 2) * (int)sizeof(T));
         o[0] = from_double<T>((double)count / (double)kd.l_out);
         o[1] = mx;
         if (MPV) o[2] = count > 0 ? from_double<T>((double)psum / (double)count) : T(0);
@@ -1169,6 +1242,8 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
   const int C = a.n_channels, L = a.l_series, H = a.halo, S = a.sstride;
   T* copy1 = copy0 + C * S;
   __shared__ int s_item, s_next;
+  if (tid == 0)
+    RK_CHK_SET(copy0, nullptr, nullptr, nullptr, a.out, reinterpret_cast<T*>(a.out) + a.n_series * a.ld_out);
   for (int k = tid; k < 2 * C * S; k += blockDim.x) copy0[k] = T(0);
   const int ngroups = (a.k_end - a.k_begin + 31) / 32;
   const T* wts = reinterpret_cast<const T*>(a.weights);
@@ -1225,6 +1300,8 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
 #pragma unroll
         for (int j = 0; j < LEN; ++j) {
           const T* xp = ((j & 1) ? q01 : q00) + j * d + tb;
+          RK_CHK_READ(xp, 4 * (int)sizeof(T));
+          RK_CHK(((uintptr_t)xp & (2 * sizeof(T) - 1)) == 0);
           acc0 = pair_tap<T>(acc0, w0[j], *reinterpret_cast<const V*>(xp), one2, false);
           acc1 = pair_tap<T>(acc1, w0[j], *reinterpret_cast<const V*>(xp + 2), one2, false);
         }
@@ -1236,6 +1313,8 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
 #pragma unroll
           for (int j = 0; j < LEN; ++j) {
             const T* xp = ((j & 1) ? q1 : q0) + j * d + tb;
+            RK_CHK_READ(xp, 4 * (int)sizeof(T));
+            RK_CHK(((uintptr_t)xp & (2 * sizeof(T) - 1)) == 0);
             const T wj = wc[j];
             acc0 = pair_tap<T>(acc0, wj, *reinterpret_cast<const V*>(xp), one2, false);
             acc1 = pair_tap<T>(acc1, wj, *reinterpret_cast<const V*>(xp + 2), one2, false);
@@ -1269,6 +1348,7 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
       }
       if (live) {
         T* o = reinterpret_cast<T*>(a.out) + i * a.ld_out + (int64_t)kd.col * a.fpk;
+        RK_CHK_WRITE(o, (MPV ? 3 : 2) * (int)sizeof(T));
         o[0] = from_double<T>((double)count / (double)kd.l_out);
         o[1] = mx;
         if (MPV) o[2] = count > 0 ? from_double<T>((double)psum / (double)count) : T(0);
@@ -1340,6 +1420,8 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
   if (tid == 0) {
     s_nan = __int_as_float(0x7fffffff);
     if (!GMEM && p.h.vec_in) mbar_init(bar, 1);
+    RK_CHK_SET(smem, GMEM ? (const void*)p.h.nanp : (const void*)&s_nan, p.h.xpad, GMEM ? p.h.nanp + 1 : nullptr,
+               p.h.out, p.h.out + p.h.n_series * p.h.ld_out);
   }
   const int C = p.h.n_channels, L = p.h.l_series, H = p.h.halo, S = p.h.sstride;
   const int SPI = p.h.spi;
@@ -1379,7 +1461,11 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         const unsigned row_bytes = (unsigned)L * 4u;
         mbar_expect_tx(bar, row_bytes * (unsigned)(ns * C));
         const float* src = p.h.x + series0 * C * L;
-        for (int r = 0; r < ns * C; ++r) tma_row(smem_u32(smem + r * S + H), src + (int64_t)r * L, row_bytes, bar);
+        for (int r = 0; r < ns * C; ++r) {
+          RK_CHK_READ(smem + r * S + H, (int)row_bytes);
+          RK_CHK(series0 + (r / C) < p.h.n_series);
+          tma_row(smem_u32(smem + r * S + H), src + (int64_t)r * L, row_bytes, bar);
+        }
       }
       mbar_wait(bar, phase);
       phase ^= 1;
