@@ -81,6 +81,9 @@ typedef struct rk_bank_info_s {
                             per 16-lane pass) in the fast-mode layout */
   int32_t n_paired_chunks; /* single-kernel chunks run position-paired (the
                                two FFMA2 lanes on two positions of the kernel) */
+  int32_t n_quarter_chunks; /* chunks laid out as quarter-warp chunks (four
+                               series per 8-lane pass) in the fast-mode layout */
+  int32_t reserved;
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

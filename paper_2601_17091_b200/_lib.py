@@ -78,6 +78,8 @@ class BankInfo(ctypes.Structure):
         ("ctas_per_sm", ctypes.c_int32),
         ("n_half_chunks", ctypes.c_int32),
         ("n_paired_chunks", ctypes.c_int32),
+        ("n_quarter_chunks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

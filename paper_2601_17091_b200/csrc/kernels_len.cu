@@ -29,14 +29,15 @@ void fill_wide(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   }
 }
 
-// half-warp chunks (single channel): PPV/MAX kernels and the fast MPV kernel
-template <int RI, int P>
-void fill_half(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
+// lane-group chunks (single channel; LG = 16 half-warp, 8 quarter-warp):
+// PPV/MAX kernels and the fast MPV kernel
+template <int RI, int P, int LG>
+void fill_group(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   constexpr int R = rk::r_of(RI);
-  wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, false, false, true>;
+  wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, false, false, LG>;
   if constexpr (R <= rk::kExactRMax) {
-    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, true, false, false, true>;
-    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, true, false, true>;
+    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, true, false, false, LG>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, P, 1, false, true, false, LG>;
   }
 }
 
@@ -45,9 +46,9 @@ template <int RI, int NC>
 void fill_sp(rk::WarpFn* wide, rk::WarpFn* mpv, int cls) {
   constexpr int R = rk::r_of(RI);
   if constexpr (R <= rk::sp_rmax(NC, RK_LEN)) {
-    wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, false, false, false, true>;
-    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, true, false, false, false, true>;
-    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, true, false, false, true>;
+    wide[2 * cls + 0] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, false, false, 32, true>;
+    wide[2 * cls + 1] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, true, false, false, 32, true>;
+    mpv[cls] = rk::rocket_wide_kernel<RK_LEN, R, 1, NC, false, true, false, 32, true>;
   }
 }
 
@@ -74,8 +75,10 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
   fill_wide<RI, 1, 2>(dt, mt, base + 1);
   fill_wide<RI, 1, 0>(dt, mt, base + 2);
   fill_wide<RI, 1, 1>(dt, mt, base + 3);
-  fill_half<RI, 2>(dt, mt, base + 4);
-  fill_half<RI, 1>(dt, mt, base + 5);
+  fill_group<RI, 2, 16>(dt, mt, base + 4);
+  fill_group<RI, 1, 16>(dt, mt, base + 5);
+  fill_group<RI, 2, 8>(dt, mt, base + 8);
+  fill_group<RI, 1, 8>(dt, mt, base + 9);
   fill_sp<RI, 1>(dt, mt, base + 6);
   fill_sp<RI, 2>(dt, mt, base + 7);
   fill_gmem<RI, 2>(gt, base + 0);

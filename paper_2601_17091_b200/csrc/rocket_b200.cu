@@ -165,10 +165,14 @@ struct rk_bank_s {
   // the same bank with the exact-mode half-warp margin (null when equal to
   // the fast-mode layout's or without half-warp chunks)
   rk_bank_s* exact_bank = nullptr;
+  // the same bank without quarter-warp chunks, for transforms whose items
+  // hold two or three series (null when the bank has no quarter-warp chunks)
+  rk_bank_s* half_bank = nullptr;
 
   ~rk_bank_s() {
     delete full_bank;
     delete exact_bank;
+    delete half_bank;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
@@ -426,6 +430,11 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   if (exact && fpk == 2 && b->exact_bank)
     return launch_wide_chain(b->exact_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
+  // two or three series per item: quarter-warp chunks cannot fill their four
+  // lane groups, so run the layout priced without them
+  if (spi < 4 && b->half_bank)
+    return launch_wide_chain(b->half_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
+                             nanp);
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
@@ -442,6 +451,8 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
       int cls = wl.cls;
       // half-warp chunks need two series per item; otherwise run their data
       // on the full-warp kernel of the same (length, R, pairs)
+      if (rk::nck_quarter(cls % rk::kNumNck) && spi < 4)
+        cls += rk::nck_as_half(cls % rk::kNumNck) - cls % rk::kNumNck;
       if (rk::nck_half(cls % rk::kNumNck) && spi < 2) cls += rk::nck_full(cls % rk::kNumNck) - cls % rk::kNumNck;
       fn = fpk == 3 ? kernel_table().mfn[exec_cls(cls, 1)] : kernel_table().dfn[2 * exec_cls(cls, exact) + exact];
     }
@@ -847,7 +858,7 @@ namespace {
 int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
                      const int32_t* paddings, const float* biases, const float* weights, const int64_t* woff,
                      const int32_t* chidx, const int64_t* choff, const int32_t* chcnt, int32_t device,
-                     int64_t half_margin, rk_bank_t* out) {
+                     int64_t half_margin, bool allow_quarter, rk_bank_t* out) {
   if (!out) return fail(RK_ERR_INVALID, "bank output pointer is NULL");
   *out = nullptr;
   if (K < 1) return fail(RK_ERR_INVALID, "bank must contain at least one kernel");
@@ -963,6 +974,10 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   const bool sp_ok = !getenv("RK_NO_SP");
   const bool half_ok = half_margin > 0 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
+  // quarter-warp chunks (8 lanes per series, four series per pass): the
+  // same rule with four staged series per CTA
+  const bool quarter_ok = half_ok && allow_quarter && !getenv("RK_NO_QUARTER") &&
+                          (int64_t)half_ctas * (4 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   std::vector<float> wpack;
   std::vector<int> chan_off;
   for (auto& kv : groups) {
@@ -1012,7 +1027,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       dc.invd = 1.0f / (float)d;
       int best_r = 0;
       int64_t best = INT64_MAX;
-      bool half = false;
+      int lanes = 32;  // 16: half-warp, 8: quarter-warp chunk
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
         if (sp) {
           if (rk::r_of(ri) > rk::sp_rmax(nc, len)) continue;
@@ -1029,21 +1044,31 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
         if (cst < best) {
           best = cst;
           best_r = ri;
-          half = false;
+          lanes = 32;
         }
         // single-channel chunks may run as half-warp chunks (two series per
-        // pass of 16-lane steps): per series, half the 16-lane step cost
+        // pass of 16-lane steps: per series, half the 16-lane step cost) or
+        // quarter-warp chunks (four series per pass of 8-lane steps)
         if (half_ok && nc == 1) {
           const int64_t fixed = 40 * 2 * P + 60;
           const int64_t c16 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 16) - fixed) / 2 + fixed;
           if (c16 * 100 < best * half_margin) {
             best = c16;
             best_r = ri;
-            half = true;
+            lanes = 16;
+          }
+          if (quarter_ok) {
+            const int64_t c8 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 8) - fixed) / 4 + fixed;
+            if (c8 * 100 < best * half_margin) {
+              best = c8;
+              best_r = ri;
+              lanes = 8;
+            }
           }
         }
       }
-      if (half) nck = nck == 0 ? 4 : 5;
+      if (lanes == 16) nck = nck == 0 ? 4 : 5;
+      if (lanes == 8) nck = nck == 0 ? 8 : 9;
       hc.cost = best;
       dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
       // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is
@@ -1288,17 +1313,24 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   const int64_t margin_fast = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   const int64_t margin_exact = getenv("RK_HALF_MARGIN_EXACT") ? atoi(getenv("RK_HALF_MARGIN_EXACT")) : 110;
   int rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
-                            margin_fast, out);
+                            margin_fast, true, out);
   if (rc) return rc;
   rk_bank_t b = *out;
   auto has_half = [](rk_bank_t x) {
+    for (const auto& wl : x->wide_launches) {
+      const int k = wl.cls % rk::kNumNck;
+      if (rk::nck_half(k) || rk::nck_quarter(k)) return true;
+    }
+    return false;
+  };
+  auto has_quarter = [](rk_bank_t x) {
     for (const auto& wl : x->wide_launches)
-      if (rk::nck_half(wl.cls % rk::kNumNck)) return true;
+      if (rk::nck_quarter(wl.cls % rk::kNumNck)) return true;
     return false;
   };
   auto twin = [&](int64_t margin, rk_bank_t* dst) -> int {
     int r = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt,
-                             device, margin, dst);
+                             device, margin, false, dst);
     if (r) {
       delete b;
       *out = nullptr;
@@ -1313,6 +1345,8 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     // R priced for 16 lanes (config 2 bank at 2,000 series: -6 % fast,
     // -11 % exact).
     if ((rc = twin(0, &b->full_bank))) return rc;
+    // items of two or three series: the layout without quarter-warp chunks
+    if (has_quarter(b) && (rc = twin(margin_fast, &b->half_bank))) return rc;
     // exact mode (FMUL2 + FFMA2 per tap) favours half-warp chunks more
     if (margin_exact != margin_fast) {
       if ((rc = twin(margin_exact, &b->exact_bank))) return rc;
@@ -1349,6 +1383,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   info->ctas_per_sm = b->wide_ctas_per_sm;
   for (const auto& hc : b->chunks) {
     info->n_half_chunks += rk::nck_half(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+    info->n_quarter_chunks += rk::nck_quarter(hc.dev.cls % rk::kNumNck) ? 1 : 0;
     info->n_paired_chunks += rk::nck_sp(hc.dev.cls % rk::kNumNck) ? 1 : 0;
   }
   if (b->wide_path)

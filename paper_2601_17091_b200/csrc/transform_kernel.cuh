@@ -79,21 +79,31 @@ __host__ __device__ constexpr int r_of(int r_idx) {
 constexpr int kExactRMax = 13;
 constexpr int kExactRIdx13 = 5;
 static_assert(r_of(kExactRIdx13) == kExactRMax, "R class table");
-constexpr int kNumNck = 8;
+constexpr int kNumNck = 10;
 // (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop.
 // 4 / 5: the 1-channel kinds 0 / 3 run as half-warp chunks (two series per
 // pass); same chunk data, so they fall back to 0 / 3 when items hold one
 // series.  6 / 7: single-kernel chunks over 1 / 2 channel slots run
 // position-paired ("SP"): the two FFMA2 lanes hold two positions of the
 // one kernel instead of a kernel and an idle zero-weight slot.
-__host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4) ? 2 : 1; }
+// 8 / 9: the 1-channel kinds 0 / 3 as quarter-warp chunks (four series per
+// pass, 8 lanes each); they run as the half-warp kinds 4 / 5 when items
+// hold two or three series.
+__host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4 || nck == 8) ? 2 : 1; }
 __host__ __device__ constexpr int nck_slots(int nck) { return (nck == 1 || nck == 7) ? 2 : nck == 2 ? 0 : 1; }
 __host__ __device__ constexpr bool nck_half(int nck) { return nck == 4 || nck == 5; }
-__host__ __device__ constexpr bool nck_sp(int nck) { return nck >= 6; }
+__host__ __device__ constexpr bool nck_quarter(int nck) { return nck == 8 || nck == 9; }
+__host__ __device__ constexpr bool nck_sp(int nck) { return nck == 6 || nck == 7; }
+// lanes per series group of a kind (32: the whole warp on one series)
+__host__ __device__ constexpr int nck_lanes(int nck) { return nck_half(nck) ? 16 : nck_quarter(nck) ? 8 : 32; }
+// the half-warp kind of a quarter-warp kind
+__host__ __device__ constexpr int nck_as_half(int nck) { return nck == 8 ? 4 : nck == 9 ? 5 : nck; }
 // largest R of the position-paired kinds (2R positions per lane: the pair
 // window and accumulators fit the ~80-register budget)
 __host__ __device__ constexpr int sp_rmax(int nc, int len) { return nc == 1 ? (len == 7 ? 9 : 7) : 5; }
-__host__ __device__ constexpr int nck_full(int nck) { return nck == 4 ? 0 : nck == 5 ? 3 : nck; }
+__host__ __device__ constexpr int nck_full(int nck) {
+  return (nck == 4 || nck == 8) ? 0 : (nck == 5 || nck == 9) ? 3 : nck;
+}
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
 // One chunk (class-kernel layout, global memory).
@@ -394,13 +404,15 @@ __device__ __forceinline__ void finish_chunk(const CH& c, Pool<G, MPV>& st, floa
   }
 }
 
-// Finish for half-warp chunks: lanes 0-15 hold series A's pools, 16-31
-// series B's; butterfly reductions inside each half, then lane g of each
-// half writes kernel g of its series (orow_b may be null: no second series).
-template <int G, bool EXACT, class CH, bool MPV = false>
-__device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G, MPV>& st, float* __restrict__ orow_a,
-                                                  float* __restrict__ orow_b, int fpk, int vec_out, int lane) {
-  const int hl = lane & 15;
+// Finish for lane-group chunks (LG = 16: half-warp, 8: quarter-warp):
+// lanes [g*LG, (g+1)*LG) hold series si + g's pools; butterfly reductions
+// inside each group, then lane k of each group writes kernel k of its
+// series (orow: the group's output row, null for a group shadowing the
+// last series, which writes nothing).
+template <int G, bool EXACT, class CH, bool MPV = false, int LG = 16>
+__device__ __forceinline__ void finish_chunk_group(const CH& c, Pool<G, MPV>& st, float* __restrict__ orow, int fpk,
+                                                   int vec_out, int lane) {
+  const int hl = lane & (LG - 1);
   unsigned my_cnt = 0;
   float my_ext = 0.0f, my_bias = 0.0f, my_ps = 0.0f;
   int my_col = 0;
@@ -411,7 +423,7 @@ __device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G, MPV>& st,
     float ps = 0.0f;
     if (MPV) ps = (g & 1) ? st.ps[g / 2].y : st.ps[g / 2].x;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
+    for (int o = LG / 2; o > 0; o >>= 1) {
       cnt += __shfl_xor_sync(kFull, cnt, o);
       const float oe = __shfl_xor_sync(kFull, e, o);
       e = EXACT ? fmaxf(e, oe) : fminf(e, oe);
@@ -425,7 +437,6 @@ __device__ __forceinline__ void finish_chunk_half(const CH& c, Pool<G, MPV>& st,
       my_ps = ps;
     }
   }
-  float* orow = lane < 16 ? orow_a : orow_b;
   if (hl < c.nk && orow) {
     const float ppv = __fdiv_rn((float)my_cnt, (float)c.n);  // == f32(RN64(count / l_out)), see finish_chunk
     const float mx = EXACT ? __fadd_rn(my_ext, my_bias) : -my_ext;
@@ -476,14 +487,14 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P, MPV>& st, const float* co
 // all complete runs go through the unmasked path; the remaining starts
 // (an incomplete 32-group and the final partial run, whose positions
 // v0 + r*d may pass n) through masked steps with clamped reads.
-// LANES = 16: a half-warp walks one series (lane is the lane in the half,
-// q32 / r32 are 16 / d and 16 % d).
+// LANES = 16 / 8: a half / quarter warp walks one series (lane is the lane
+// in its group, q32 / r32 are LANES / d and LANES % d).
 template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, int LANES = 32>
 __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
                                               int r32, float invd, const float* nan_slot, int lane) {
-  constexpr int kLog = LANES == 32 ? 5 : 4;
+  constexpr int kLog = LANES == 32 ? 5 : LANES == 16 ? 4 : 3;
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
@@ -1405,7 +1416,7 @@ __device__ __forceinline__ void tma_row(unsigned dst, const void* src, unsigned 
                : "memory");
 }
 
-template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false, bool HALF = false,
+template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, bool GMEM = false, int LG = 32,
           bool SP = false>
 __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(const __grid_constant__ WParams p) {
   extern __shared__ __align__(16) float smem[];
@@ -1503,7 +1514,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
         const float2* wp = reinterpret_cast<const float2*>(wbase + (size_t)ci * p.h.wbytes);
         if constexpr (SP) {
           // position-paired single-kernel chunk: the host packed (w, w)
-          static_assert(P == 1 && !HALF && !GMEM, "position-paired chunks: one kernel, full warp, staged series");
+          static_assert(P == 1 && LG == 32 && !GMEM, "position-paired chunks: one kernel, full warp, staged series");
           float ws[NC][LEN];
 #pragma unroll
           for (int s = 0; s < NC; ++s)
@@ -1533,27 +1544,31 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           for (int q = 0; q < P; ++q)
 #pragma unroll
             for (int j = 0; j < LEN; ++j) w[s][q][j] = wp[(s * P + q) * LEN + j];
-        if constexpr (HALF) {
-          // half-warp chunks: two series per pass, 16 lanes each (finer
-          // step granularity for short position ranges); an odd last series
-          // is shadowed by the upper half, which writes nothing
-          static_assert(!GMEM && !(MPV && EXACT), "half-warp chunks: staged series; MPV in fast mode");
-          const int half = lane >> 4, hl = lane & 15;
-          const int q16 = c.q32 >> 1, r16 = 16 - q16 * c.d;
-          for (int si = 0; si < ns; si += 2) {
-            const int sj = min(si + half, ns - 1);
+        if constexpr (LG < 32) {
+          // lane-group chunks: 32 / LG series per pass, LG lanes each
+          // (finer step granularity for short position ranges); groups past
+          // the last series shadow it and write nothing
+          static_assert(!GMEM && !(MPV && EXACT), "lane-group chunks: staged series; MPV in fast mode");
+          constexpr int NG = 32 / LG;
+          const int grp = lane >> (LG == 16 ? 4 : 3), hl = lane & (LG - 1);
+          const int qg = c.q32 >> (NG == 2 ? 1 : 2), rg = LG - qg * c.d;  // LG / d, LG % d
+          for (int si = 0; si < ns; si += NG) {
+            const int sj = min(si + grp, ns - 1);
             const float* sx = sbase + sj * slot + H;
             const float* chan[NC];
 #pragma unroll
             for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
             Pool<2 * P, MPV> st;
             pool_init<2 * P, EXACT, MPV>(st);
-            run_positions<LEN, R, P, NC, EXACT, MPV, 16>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, q16, r16,
+            run_positions<LEN, R, P, NC, EXACT, MPV, LG>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, qg, rg,
                                                          c.invd, nanp, hl);
-            float* orow_a = p.h.out + (series0 + si) * p.h.ld_out;
-            finish_chunk_half<2 * P, EXACT, WChunk, MPV>(c, st, orow_a, si + 1 < ns ? orow_a + p.h.ld_out : nullptr,
-                                                         p.h.fpk, p.h.vec_out, lane);
-            done += (unsigned long long)c.nk * (unsigned long long)c.n * (si + 1 < ns ? 2u : 1u);
+            float* orow0 = p.h.out + (series0 + si) * p.h.ld_out;
+            float* orow = orow0;
+#pragma unroll
+            for (int g = 1; g < NG; ++g)
+              if (grp == g) orow = si + g < ns ? orow0 + g * p.h.ld_out : nullptr;
+            finish_chunk_group<2 * P, EXACT, WChunk, MPV, LG>(c, st, orow, p.h.fpk, p.h.vec_out, lane);
+            done += (unsigned long long)c.nk * (unsigned long long)c.n * (unsigned)min(NG, ns - si);
           }
           continue;
         }
