@@ -421,6 +421,21 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   while (spi < spi_max && n >= min_items * (spi + 1) * st->sms * ctas &&
          (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
     ++spi;
+  // whole passes of the lane groups: no shadowed groups in the last pass of
+  // an item (a 6-series item on quarter-warp chunks wasted 1/4 of a pass:
+  // config 2 at 4 CTAs 240k -> 314k series/s); RK_SPI_ROUND=0 disables
+  static const bool spi_round = !getenv("RK_SPI_ROUND") || atoi(getenv("RK_SPI_ROUND"));
+  if (spi_round) {
+    bool q = false, h = false;
+    for (const auto& wl : b->wide_launches) {
+      q |= rk::nck_quarter(wl.cls % rk::kNumNck);
+      h |= rk::nck_half(wl.cls % rk::kNumNck);
+    }
+    if (q && spi >= 4)
+      spi &= ~3;
+    else if ((q || h) && spi >= 2)
+      spi &= ~1;
+  }
   // one series per item: half-warp chunks cannot pair series, so run the
   // bank's full-warp twin
   if (spi < 2 && b->full_bank)
@@ -968,9 +983,16 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   // otherwise items hold one series and the half classes would only run
   // their chunks on the full-warp kernel at an R priced for 16 lanes: 3
   // channels x L = 2048, 4 CTAs per SM, measured 0.4 % / 1.3 % slower)
+  // CTAs per SM on the wide path (RK_WIDE_CTAS overrides): 3 x 8 warps, or
+  // 2 x 12 for series of >= 32 KB staged (r02 sweeps, profiles/r02_cta_sweep.txt:
+  // FordA shape +12 %, L = 2048 +2.6 %, config 5 +1.5 % against 6 x 4 and
+  // 4 x 6; config 2 unchanged); 6 x 4 for series read from global memory
+  const int cta_cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS")))
+                      : gmem                 ? 6
+                      : smem >= 32768        ? 2
+                                             : 3;
   const int half_ctas = std::min<int>(
-      std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))),
-      getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6);
+      std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))), cta_cap);
   const bool sp_ok = !getenv("RK_NO_SP");
   const bool half_ok = half_margin > 0 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
@@ -1148,13 +1170,12 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   for (size_t i = 0; i < b->chunks.size(); ++i) b->cost_prefix[i + 1] = b->cost_prefix[i] + b->chunks[i].cost;
 
   // Wide path (every bank; fixed slots for 1-2 channels, the run-time slot
-  // loop beyond).  CTAs per SM as shared memory allows (at most 6: 6 x 4
-  // warps with up to 8 series per item measured best at L = 1024), warps per
-  // CTA so the SM holds 24 warps (the ~80-register budget).
+  // loop beyond).  CTAs per SM as shared memory allows, at most cta_cap;
+  // warps per CTA so the SM holds 24 warps (the ~80-register budget).
   {
     const int per_cta = (gmem ? 0 : (int)smem) + 1024;  // + the per-CTA reservation
     const int by_smem = std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / per_cta));
-    const int cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS"))) : 6;
+    const int cap = cta_cap;
     if (by_smem >= 1 && wide_ok) {
       b->wide_path = true;
       b->wide_ctas_smem = by_smem;
