@@ -987,8 +987,11 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   // 2 x 12 for series of >= 32 KB staged (r02 sweeps, profiles/r02_cta_sweep.txt:
   // FordA shape +12 %, L = 2048 +2.6 %, config 5 +1.5 % against 6 x 4 and
   // 4 x 6; config 2 unchanged); 6 x 4 for series read from global memory
+  // Small banks (< 2,000 kernels: few chunks per launch) keep narrower CTAs,
+  // so no warp idles on an item (config 5 at 1k kernels: 2 x 12 was 4.5 %
+  // slower than 4 x 6).
   const int cta_cap = getenv("RK_WIDE_CTAS") ? std::max(1, atoi(getenv("RK_WIDE_CTAS")))
-                      : gmem                 ? 6
+                      : gmem || K < 2000     ? 6
                       : smem >= 32768        ? 2
                                              : 3;
   const int half_ctas = std::min<int>(
