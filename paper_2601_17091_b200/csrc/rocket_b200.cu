@@ -451,6 +451,10 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
     return launch_wide_chain(b->half_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
+  if (profile)
+    fprintf(stderr, "RK_PROFILE chain n=%lld spi=%d ctas=%d warps=%d launches=%zu twins(full=%d exact=%d half=%d)\n",
+            (long long)n, spi, ctas, warps, b->wide_launches.size(), b->full_bank != nullptr,
+            b->exact_bank != nullptr, b->half_bank != nullptr);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
@@ -1352,9 +1356,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
       if (rk::nck_quarter(wl.cls % rk::kNumNck)) return true;
     return false;
   };
-  auto twin = [&](int64_t margin, rk_bank_t* dst) -> int {
+  auto twin = [&](int64_t margin, rk_bank_t* dst, bool quarter = false) -> int {
     int r = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt,
-                             device, margin, false, dst);
+                             device, margin, quarter, dst);
     if (r) {
       delete b;
       *out = nullptr;
@@ -1372,12 +1376,16 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     // items of two or three series: the layout without quarter-warp chunks
     if (has_quarter(b) && (rc = twin(margin_fast, &b->half_bank))) return rc;
     // exact mode (FMUL2 + FFMA2 per tap) favours half-warp chunks more
+    // (quarter-warp chunks included: FordA shape exact 330k -> 354k series/s),
+    // with its own half-warp twin for items of two or three series
     if (margin_exact != margin_fast) {
-      if ((rc = twin(margin_exact, &b->exact_bank))) return rc;
+      if ((rc = twin(margin_exact, &b->exact_bank, true))) return rc;
       if (!has_half(b->exact_bank)) {
         b->device_bytes -= b->exact_bank->device_bytes;
         delete b->exact_bank;
         b->exact_bank = nullptr;
+      } else if (has_quarter(b->exact_bank)) {
+        if ((rc = twin(margin_exact, &b->exact_bank->half_bank))) return rc;
       }
     }
   }
