@@ -1005,6 +1005,10 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   // quarter-warp chunks (8 lanes per series, four series per pass): the
   // same rule with four staged series per CTA
+  // margin of a quarter-warp option over the best so far (RK_QUARTER_MARGIN,
+  // percent; default: the half-warp margin)
+  const int64_t quarter_margin =
+      getenv("RK_QUARTER_MARGIN") ? atoi(getenv("RK_QUARTER_MARGIN")) : half_margin;
   const bool quarter_ok = half_ok && allow_quarter && !getenv("RK_NO_QUARTER") &&
                           (int64_t)half_ctas * (4 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   std::vector<float> wpack;
@@ -1088,7 +1092,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
           }
           if (quarter_ok) {
             const int64_t c8 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 8) - fixed) / 4 + fixed;
-            if (c8 * 100 < best * half_margin) {
+            if (c8 * 100 < best * quarter_margin) {
               best = c8;
               best_r = ri;
               lanes = 8;
