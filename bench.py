@@ -36,6 +36,9 @@ if ROOT not in sys.path:
 import numpy as np  # noqa: E402
 
 CONFIGS = {
+    "config1": dict(n=3_601, c=1, l=500, k=10_000, scaling="weak",
+                    workload="ROCKET transform + ridge fit/predict, 10,000 kernels, 3,601 labelled series x "
+                             "length 500 (FordA shape, synth_two_class)"),
     "config2": dict(n=100_000, c=1, l=1024, k=10_000, scaling="weak",
                     workload="ROCKET transform, 10,000 kernels, 100,000 series x length 1,024 per GPU"),
     "config3": dict(n=1_000_000, c=1, l=1024, k=10_000, scaling="strong",
@@ -251,6 +254,22 @@ def run_reference(args, cfg):
     orc.build()
     bank = generate_bank(cfg["l"], cfg["c"], cfg["k"], GenOptions(seed=0), native=False)
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    if args.config == "config1":
+        # configs[0]: the whole CPU pipeline (transform + ridge) per step
+        runs = [cpu_config1(bank, cfg) for _ in range(max(1, args.steps))]
+        total = sum(r["seconds"] for r in runs)
+        value = cfg["n"] * len(runs) / total
+        line = {"impl": "reference", "metric": "ROCKET transform + ridge fit series/sec (FordA shape, 10k kernels)",
+                "value": value, "unit": "series/s", "n_gpus": world, "steps": len(runs), "warmup": 0,
+                "ms_per_step": 1e3 * total / len(runs), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 transform, f64 ridge",
+                "data": "synthetic: synth_two_class(1801, 500, seed=1)[:3601] with its labels",
+                "config": {"workload": cfg["workload"], "series": cfg["n"], "parallelism": "cpu threads"},
+                "cpu_baseline": {"value": value, "unit": "series/s", "cores": threads, "kind": "port",
+                                 "sample": "the whole pipeline per step", "host_cpu": host_cpu()},
+                "e2e": {"value": value, "unit": "series/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     # one step = a bounded sample sized for ~2.5 s of CPU work
     rate, _, _, _ = cpu_sample_rate(bank, cfg, 2.5)
     m = max(threads, int(rate * 2.5 // threads) * threads)
@@ -287,6 +306,127 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def config1_data(cfg):
+    """BASELINE configs[0]: synth_two_class(1801, 500, seed=1)[:3601] (SURVEY
+    §8d), labels included."""
+    from paper_2601_17091_b200 import synth_two_class
+
+    ds = synth_two_class((cfg["n"] + 1) // 2, cfg["l"], seed=1)
+    return ds.values[: cfg["n"]], ds.labels[: cfg["n"]]
+
+
+def cpu_config1(bank, cfg):
+    """The whole config-1 pipeline on the host cores: the C port of the
+    transform (all threads) + the numpy/LAPACK restatement of the
+    reference's ridge.fit and predict (oracle/ridge_oracle.py)."""
+    import oracle.oracle as orc
+    from oracle import ridge_oracle
+
+    values, labels = config1_data(cfg)
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    orc.oracle_transform(values[:threads], bank, nthreads=threads)  # warm
+    t0 = time.perf_counter()
+    feats = orc.oracle_transform(values, bank, nthreads=threads)
+    t1 = time.perf_counter()
+    model = ridge_oracle.fit(feats, labels, alpha=1.0)
+    pred = ridge_oracle.predict(model, feats)
+    t2 = time.perf_counter()
+    acc = float(np.mean(pred == np.asarray(labels)))
+    return {"seconds": t2 - t0, "transform_s": t1 - t0, "ridge_s": t2 - t1, "threads": threads,
+            "train_accuracy": acc, "value": len(labels) / (t2 - t0)}
+
+
+def run_config1(args, cfg):
+    """configs[0] on the GPU: transform (features stay in HBM) + ridge fit +
+    predict per step; the CPU leg runs the same pipeline on the host."""
+    import torch
+
+    from paper_2601_17091_b200 import GenOptions, device_bank, generate_bank, ridge
+
+    torch.cuda.set_device(0)
+    values, labels = config1_data(cfg)
+    n = len(labels)
+    bank = generate_bank(cfg["l"], cfg["c"], cfg["k"], GenOptions(seed=0))
+    db = device_bank(bank, 0)
+    info = db.info
+    x_host = torch.from_numpy(values).pin_memory()
+    x_dev = x_host.cuda()
+    feats = torch.empty((n, 2 * bank.count), device="cuda")
+    stream = torch.cuda.current_stream()
+    expected = None
+    from paper_2601_17091_b200.engine import expected_dot_products
+
+    expected = expected_dot_products(bank, n)
+    stages = {}
+
+    def step(xd, timed_stages=False):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        ex = db.transform_into(xd.data_ptr(), n, feats.data_ptr(), feats.shape[1], mode=args.mode,
+                               stream=stream.cuda_stream)
+        e[1].record(stream)
+        model = ridge.fit(feats, labels, alpha=1.0)
+        e[2].record(stream)
+        pred = ridge.predict(model, feats)  # labels on the host
+        e[3].record(stream)
+        if timed_stages:
+            torch.cuda.synchronize()
+            stages.update(transform_ms=e[0].elapsed_time(e[1]), ridge_fit_ms=e[1].elapsed_time(e[2]),
+                          predict_ms=e[2].elapsed_time(e[3]))
+        if ex != expected:
+            raise RuntimeError("executed positions differ from expected_dot_products")
+        return pred
+
+    for _ in range(args.warmup):
+        step(x_dev)
+    pred = step(x_dev, timed_stages=True)
+    acc = float(np.mean(pred == np.asarray(labels)))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(x_dev)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    value = n * args.steps / (ms / 1e3)
+    # e2e: the series from pinned host memory each step, predictions read back
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        xd = x_host.to("cuda", non_blocking=True)
+        step(xd)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    cpu = None
+    if not args.no_cpu:
+        import oracle.oracle as orc
+
+        orc.build()
+        c = cpu_config1(bank, cfg)
+        cpu = {"value": c["value"], "unit": "series/s", "cores": c["threads"], "kind": "port",
+               "sample": f"the whole config-1 pipeline ({n} series): transform {c['transform_s']:.1f} s (C port of "
+                         f"engine._run_batch) + ridge fit/predict {c['ridge_s']:.2f} s (numpy/LAPACK restatement "
+                         f"of ridge.py:100-197)", "train_accuracy": c["train_accuracy"], "host_cpu": host_cpu()}
+    flops = info["useful_flops_per_series"] * n / (stages["transform_ms"] / 1e3) / 1e12
+    line = {
+        "metric": "ROCKET transform + ridge fit series/sec (FordA shape, 10k kernels)", "value": value,
+        "unit": "series/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 transform, f64 ridge",
+        "mode": args.mode, "data": "synthetic: synth_two_class(1801, 500, seed=1)[:3601] with its labels",
+        "config": {"workload": cfg["workload"], "series": n, "l_series": cfg["l"], "n_kernels": bank.count,
+                   "ridge": "fp64 one-vs-rest, dual Cholesky on the GPU (features never leave HBM)"},
+        "stages": stages, "train_accuracy": acc,
+        "roofline": {"bound": "fp32", "achieved": flops, "peak": FP32_PEAK_MEASURED, "unit": "TFLOP/s",
+                     "frac": flops / FP32_PEAK_MEASURED, "traffic": None,
+                     "kernel": "rocket_wide_kernel (the transform stage; the ridge stage is cuBLAS/cuSOLVER fp64)"},
+        "e2e": {"value": n * args.steps / dt, "unit": "series/s", "h2d_bytes_per_step": int(x_host.numel() * 4),
+                "d2h_bytes_per_step": int(n * 8), "ms_per_step": 1e3 * dt / args.steps},
+        "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(info["n_launches"]) * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = dict(CONFIGS[args.config])
@@ -296,6 +436,8 @@ def main():
         cfg["n"] = args.series
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.config == "config1":
+        return run_config1(args, cfg)
 
     import torch
     import torch.distributed as dist

@@ -128,3 +128,17 @@ def test_model_file_roundtrip_matches_reference(name, tmp_path):
     (tmp_path / "t.rkrm").write_bytes(raw[:-3])
     with pytest.raises(FormatError):
         ridge.RidgeModel.load(tmp_path / "t.rkrm")
+
+
+@pytest.mark.parametrize("name", ["dual", "primal"])
+def test_ridge_oracle_matches_reference(gold, name):
+    """The CPU restatement bench.py's config-1 baseline times (oracle/
+    ridge_oracle.py) against the reference's own fits."""
+    from oracle import ridge_oracle
+
+    feats = gold[f"{name}/features"]
+    labels = [str(v) for v in gold["labels"]]
+    m = ridge_oracle.fit(feats, labels, alpha=1.0)
+    np.testing.assert_allclose(m[0], gold[f"{name}/weights"], rtol=1e-8, atol=1e-11)
+    np.testing.assert_allclose(m[1], gold[f"{name}/intercepts"], rtol=0, atol=0)
+    assert [int(v) for v in ridge_oracle.predict(m, feats)] == gold[f"{name}/predict"].tolist()
