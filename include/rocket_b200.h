@@ -128,7 +128,9 @@ int rk_bank_info(rk_bank_t bank, rk_bank_info_t* info);
  * order, bit-identical).  Fast-mode MPV sums the positive outputs per lane
  * and then across the warp (within 1e-5 relative).  x and out may be host or
  * device pointers.  stream is a
- * cudaStream_t (NULL = the library's per-device stream); for device x and
+ * cudaStream_t (NULL = the caller's default stream: the transform runs on the
+ * library's per-device stream, ordered after the work already queued on the
+ * default stream and before the work queued there later); for device x and
  * out the call is asynchronous on that stream, otherwise it returns after
  * the features are in out.  *executed (may be NULL) receives the number of
  * dot-product positions evaluated, counted on the device; it equals

@@ -1451,8 +1451,18 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
   const int64_t row_in = (int64_t)b->C * b->L;
   if (dx && dout) {
     // Device-resident: asynchronous on the caller's stream (or the
-    // library's); the counters live in that stream's scratch block.
+    // library's); the counters live in that stream's scratch block.  A NULL
+    // stream means the caller's default (legacy) stream: the library stream
+    // is non-blocking, so it waits for the work already queued there (e.g.
+    // the H2D copy of x) and the default stream waits for the transform.
     cudaStream_t stream = stream_ptr ? (cudaStream_t)stream_ptr : st->stream;
+    cudaEvent_t ev_in = nullptr;
+    if (!stream_ptr) {
+      RK_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+      RK_CUDA(cudaEventRecord(ev_in, (cudaStream_t)0));
+      RK_CUDA(cudaStreamWaitEvent(stream, ev_in, 0));
+      RK_CUDA(cudaEventDestroy(ev_in));
+    }
     std::mutex* smu = nullptr;
     {
       std::lock_guard<std::mutex> lk(st->pool_mu);
@@ -1468,6 +1478,13 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
     rc = launch(b, st, x, n, out + row0 * ld_out * esz, ld_out, fpk, mode, stream, d_exec,
                 reinterpret_cast<int*>(d_exec + 1), esz);
     if (rc) return rc;
+    if (!stream_ptr) {
+      cudaEvent_t ev_out = nullptr;
+      RK_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+      RK_CUDA(cudaEventRecord(ev_out, stream));
+      RK_CUDA(cudaStreamWaitEvent((cudaStream_t)0, ev_out, 0));
+      RK_CUDA(cudaEventDestroy(ev_out));
+    }
     if (executed) {
       unsigned long long h = 0;
       RK_CUDA(cudaMemcpyAsync(&h, d_exec, sizeof(h), cudaMemcpyDeviceToHost, stream));

@@ -209,3 +209,21 @@ def test_run_batch_mode_dropin(mode, cuda_ready):
         check_fast(out[rows], ref, x[rows], bank)
     assert lib.rk_run_batch_f32_mode(p(x), n, 1, 1024, *[p(a) for a in arrs], bank.count, 1024, 2, p(out),
                                      out.shape[1], 0, 7) < 0
+
+
+def test_default_stream_ordering(cuda_ready):
+    """stream=None means the caller's default stream: an asynchronous H2D of
+    x queued there must land before the transform reads it, and default-stream
+    work queued after the call sees the features (bench config 1's e2e leg)."""
+    import torch
+
+    bank = generate_bank(500, 1, 2000, GenOptions(seed=0))
+    values = synth_random(3601, 1, 500, seed=1).values
+    db = device_bank(bank, 0)
+    ref, _ = _device_transform(db, torch.from_numpy(values).cuda(), len(values), 2, "exact")
+    x_host = torch.from_numpy(values).pin_memory()
+    for _ in range(3):
+        xd = x_host.to("cuda", non_blocking=True)  # queued on the default stream
+        out = torch.full((len(values), bank.count * 2), float("nan"), device="cuda")
+        db.transform_into(xd.data_ptr(), len(values), out.data_ptr(), out.shape[1], mode="exact")
+        assert torch.equal(out, ref)  # default-stream comparison after the call
