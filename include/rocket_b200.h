@@ -232,7 +232,9 @@ int rk_transform_stream(rk_bank_t bank, int32_t in_fd, int64_t in_offset,
  * Per-kernel outputs have count entries; channel_indices and weights are
  * filled up to index_capacity / weight_capacity (count*n_channels and
  * count*11*n_channels always suffice) and *n_indices / *n_weights receive
- * the lengths used.  Returns RK_ERR_CAPACITY if a buffer is too small. */
+ * the lengths used.  Returns RK_ERR_CAPACITY if a buffer is too small — with
+ * the lengths needed in *n_indices / *n_weights, so a caller can size its
+ * buffers from an estimate and call again (the draw is deterministic). */
 int rk_generate_bank(int64_t count, int32_t l_series, int32_t n_channels,
                      uint64_t seed, int32_t center_weights,
                      const double* exponent_bounds, double channel_bound,

@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 namespace {
@@ -232,7 +233,14 @@ extern "C" int rk_generate_bank(int64_t count, int32_t l_series, int32_t n_chann
     return rk_set_error(RK_ERR_INVALID, "NULL argument");
   Philox g(seed);
   std::vector<int64_t> picks;
-  int64_t wpos = 0, ipos = 0;
+  // the variable-length streams are drawn into exact-size buffers, then
+  // copied out; a caller buffer that is too small gets RK_ERR_CAPACITY with
+  // the sizes needed in *n_weights / *n_indices (the caller can size its
+  // buffers from an estimate and retry: the draw is deterministic)
+  std::vector<int32_t> idx;
+  std::vector<double> wts;
+  idx.reserve((size_t)count);
+  wts.reserve((size_t)count * 11);
   for (int64_t k = 0; k < count; ++k) {
     const int li = (int)bounded(g, 2);
     const int lk = kLengths[li];
@@ -242,16 +250,14 @@ extern "C" int rk_generate_bank(int64_t count, int32_t l_series, int32_t n_chann
       nsel = std::min<int64_t>(std::max<int64_t>((int64_t)std::pow(2.0, u), 1), n_channels);
       choice_without_replacement(g, n_channels, nsel, picks);
       std::sort(picks.begin(), picks.end());
-      if (ipos + nsel > index_capacity) return rk_set_error(RK_ERR_CAPACITY, "channel index buffer too small");
-      for (int64_t c = 0; c < nsel; ++c) channel_indices[ipos + c] = (int32_t)picks[(size_t)c];
+      for (int64_t c = 0; c < nsel; ++c) idx.push_back((int32_t)picks[(size_t)c]);
     } else {
-      if (ipos + 1 > index_capacity) return rk_set_error(RK_ERR_CAPACITY, "channel index buffer too small");
-      channel_indices[ipos] = 0;
+      idx.push_back(0);
     }
     const int64_t nw = nsel * lk;
-    if (wpos + nw > weight_capacity) return rk_set_error(RK_ERR_CAPACITY, "weight buffer too small");
-    double* w = weights + wpos;
-    for (int64_t j = 0; j < nw; ++j) w[j] = standard_normal(g);
+    const size_t w0 = wts.size();
+    for (int64_t j = 0; j < nw; ++j) wts.push_back(standard_normal(g));
+    double* w = wts.data() + w0;
     if (center_weights) {
       const double mean = pairwise_sum(w, nw) / (double)nw;
       for (int64_t j = 0; j < nw; ++j) w[j] = w[j] - mean;
@@ -264,10 +270,12 @@ extern "C" int rk_generate_bank(int64_t count, int32_t l_series, int32_t n_chann
     dilations[k] = d;
     paddings[k] = p;
     channel_counts[k] = (int32_t)nsel;
-    wpos += nw;
-    ipos += nsel;
   }
-  *n_weights = wpos;
-  *n_indices = ipos;
+  *n_weights = (int64_t)wts.size();
+  *n_indices = (int64_t)idx.size();
+  if ((int64_t)idx.size() > index_capacity || (int64_t)wts.size() > weight_capacity)
+    return rk_set_error(RK_ERR_CAPACITY, "channel index / weight buffer too small (sizes needed in n_indices / n_weights)");
+  std::memcpy(channel_indices, idx.data(), idx.size() * sizeof(int32_t));
+  std::memcpy(weights, wts.data(), wts.size() * sizeof(double));
   return RK_OK;
 }

@@ -66,3 +66,30 @@ def test_native_default_and_errors():
     lib = _lib.load()
     assert lib.rk_generate_bank(0, 64, 1, 0, 1, None, 0.0, *([None] * 6), 0, None, 0, None, None) == \
         _lib.RK_ERR_INVALID
+
+
+def test_native_capacity_retry_reports_sizes():
+    """A too-small buffer gets RK_ERR_CAPACITY with the exact sizes needed
+    (the caller's retry then yields the same bank as numpy)."""
+    import ctypes
+
+    from paper_2601_17091_b200 import _lib
+    from paper_2601_17091_b200.kernels import CANDIDATE_LENGTHS, dilation_exponent_bound
+
+    lib = _lib.load()
+    count, L, C = 50, 64, 40
+    bounds = np.array([dilation_exponent_bound(L, lk) for lk in CANDIDATE_LENGTHS], dtype=np.float64)
+    outs = [np.empty(count, np.int32), np.empty(count), np.empty(count, np.int32), np.empty(count, np.int32),
+            np.empty(count, np.int32)]
+    idx = np.empty(1, np.int32)
+    w = np.empty(1)
+    n_w, n_i = ctypes.c_int64(0), ctypes.c_int64(0)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rc = lib.rk_generate_bank(count, L, C, ctypes.c_uint64(9), 1, p(bounds), float(np.log2(C)), *[p(a) for a in outs],
+                              p(idx), idx.size, p(w), w.size, ctypes.byref(n_w), ctypes.byref(n_i))
+    assert rc == _lib.RK_ERR_CAPACITY
+    ref = generate_bank(L, C, count, GenOptions(seed=9), native=False)
+    assert n_i.value == ref.channel_indices.size and n_w.value == ref.weights.size
+    nat = generate_bank(L, C, count, GenOptions(seed=9), native=True)
+    assert nat.weights.tobytes() == ref.weights.tobytes()
+    assert nat.channel_indices.tobytes() == ref.channel_indices.tobytes()
