@@ -83,7 +83,8 @@ typedef struct rk_bank_info_s {
                                two FFMA2 lanes on two positions of the kernel) */
   int32_t n_quarter_chunks; /* chunks laid out as quarter-warp chunks (four
                                series per 8-lane pass) in the fast-mode layout */
-  int32_t reserved;
+  int32_t n_eighth_chunks;  /* chunks laid out as eighth-warp chunks (eight
+                               series per 4-lane pass) in the fast-mode layout */
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

@@ -79,7 +79,7 @@ class BankInfo(ctypes.Structure):
         ("n_half_chunks", ctypes.c_int32),
         ("n_paired_chunks", ctypes.c_int32),
         ("n_quarter_chunks", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("n_eighth_chunks", ctypes.c_int32),
     ]
 
 

@@ -79,6 +79,8 @@ void fill_r(rk::KernelFn* ct, rk::WarpFn* dt, rk::WarpFn* mt, rk::WarpFn* gt) {
   fill_group<RI, 1, 16>(dt, mt, base + 5);
   fill_group<RI, 2, 8>(dt, mt, base + 8);
   fill_group<RI, 1, 8>(dt, mt, base + 9);
+  fill_group<RI, 2, 4>(dt, mt, base + 10);
+  fill_group<RI, 1, 4>(dt, mt, base + 11);
   fill_sp<RI, 1>(dt, mt, base + 6);
   fill_sp<RI, 2>(dt, mt, base + 7);
   fill_gmem<RI, 2>(gt, base + 0);

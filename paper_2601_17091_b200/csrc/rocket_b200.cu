@@ -161,18 +161,20 @@ struct rk_bank_s {
   std::atomic<bool> f64_ready{false};  // d_cw64 / d_cb64 filled (rk_bank_attach_f64)
   // the same bank without half-warp chunks, for transforms whose items hold
   // one series (null when the bank has no half-warp chunks)
-  rk_bank_s* full_bank = nullptr;
-  // the same bank with the exact-mode half-warp margin (null when equal to
-  // the fast-mode layout's or without half-warp chunks)
+  // the same bank limited to 1 / 2 / 4 series per pass (narrow[0]: no lane
+  // groups — items of one series; narrow[1]: up to half-warp chunks —
+  // items of two or three series; narrow[2]: up to quarter-warp chunks —
+  // items of four to seven series); null when not narrower than this layout
+  rk_bank_s* narrow[3] = {};
+  // the same bank with the exact-mode lane-group margin (null when equal to
+  // the fast-mode layout's or without lane-group chunks)
   rk_bank_s* exact_bank = nullptr;
-  // the same bank without quarter-warp chunks, for transforms whose items
-  // hold two or three series (null when the bank has no quarter-warp chunks)
-  rk_bank_s* half_bank = nullptr;
+  // largest series per pass of any chunk of this layout (1, 2, 4, 8)
+  int max_groups = 1;
 
   ~rk_bank_s() {
-    delete full_bank;
+    for (auto* t : narrow) delete t;
     delete exact_bank;
-    delete half_bank;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
@@ -425,36 +427,30 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   // an item (a 6-series item on quarter-warp chunks wasted 1/4 of a pass:
   // config 2 at 4 CTAs 240k -> 314k series/s); RK_SPI_ROUND=0 disables
   static const bool spi_round = !getenv("RK_SPI_ROUND") || atoi(getenv("RK_SPI_ROUND"));
-  if (spi_round) {
-    bool q = false, h = false;
-    for (const auto& wl : b->wide_launches) {
-      q |= rk::nck_quarter(wl.cls % rk::kNumNck);
-      h |= rk::nck_half(wl.cls % rk::kNumNck);
-    }
-    if (q && spi >= 4)
-      spi &= ~3;
-    else if ((q || h) && spi >= 2)
-      spi &= ~1;
-  }
-  // one series per item: half-warp chunks cannot pair series, so run the
+  int pow2 = 1;  // largest power of two <= spi (series per pass an item can fill)
+  while (pow2 * 2 <= spi && pow2 < 8) pow2 *= 2;
+  if (spi_round && b->max_groups > 1) spi -= spi % std::min(b->max_groups, pow2);
+  // one series per item: lane-group chunks cannot pair series, so run the
   // bank's full-warp twin
-  if (spi < 2 && b->full_bank)
-    return launch_wide_chain(b->full_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
+  if (spi < 2 && b->narrow[0])
+    return launch_wide_chain(b->narrow[0], st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
-  // exact mode: the layout priced with its own half-warp margin
+  // exact mode: the layout priced with its own lane-group margin
   if (exact && fpk == 2 && b->exact_bank)
     return launch_wide_chain(b->exact_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
                              nanp);
-  // two or three series per item: quarter-warp chunks cannot fill their four
-  // lane groups, so run the layout priced without them
-  if (spi < 4 && b->half_bank)
-    return launch_wide_chain(b->half_bank, st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
-                             nanp);
+  // items that cannot fill the widest groups of this layout: the layout
+  // priced without them
+  if (pow2 < b->max_groups) {
+    const int j = pow2 >= 4 ? 2 : pow2 >= 2 ? 1 : 0;
+    if (b->narrow[j])
+      return launch_wide_chain(b->narrow[j], st, d_x, n, d_out, ld_out, fpk, mode, stream, d_exec, d_counters, xpad,
+                               nanp);
+  }
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
   if (profile)
-    fprintf(stderr, "RK_PROFILE chain n=%lld spi=%d ctas=%d warps=%d launches=%zu twins(full=%d exact=%d half=%d)\n",
-            (long long)n, spi, ctas, warps, b->wide_launches.size(), b->full_bank != nullptr,
-            b->exact_bank != nullptr, b->half_bank != nullptr);
+    fprintf(stderr, "RK_PROFILE chain n=%lld spi=%d ctas=%d warps=%d launches=%zu max_groups=%d exact_twin=%d\n",
+            (long long)n, spi, ctas, warps, b->wide_launches.size(), b->max_groups, b->exact_bank != nullptr);
   std::vector<cudaEvent_t> evs;
   for (size_t li = 0; li < b->wide_launches.size(); ++li) {
     const auto& wl = b->wide_launches[li];
@@ -470,9 +466,13 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
       int cls = wl.cls;
       // half-warp chunks need two series per item; otherwise run their data
       // on the full-warp kernel of the same (length, R, pairs)
-      if (rk::nck_quarter(cls % rk::kNumNck) && spi < 4)
-        cls += rk::nck_as_half(cls % rk::kNumNck) - cls % rk::kNumNck;
-      if (rk::nck_half(cls % rk::kNumNck) && spi < 2) cls += rk::nck_full(cls % rk::kNumNck) - cls % rk::kNumNck;
+      // (without a twin) run lane groups the item cannot fill on the next
+      // narrower kind of the same (length, R, pairs)
+      while (rk::nck_groups(cls % rk::kNumNck) > std::max(1, spi)) {
+        const int k = cls % rk::kNumNck;
+        const int narrower = (k == 10) ? 8 : (k == 11) ? 9 : (k == 8) ? 4 : (k == 9) ? 5 : rk::nck_full(k);
+        cls += narrower - k;
+      }
       fn = fpk == 3 ? kernel_table().mfn[exec_cls(cls, 1)] : kernel_table().dfn[2 * exec_cls(cls, exact) + exact];
     }
     if (!fn) return fail(RK_ERR_UNSUPPORTED, "no wide kernel for class %d", wl.cls);
@@ -873,11 +873,12 @@ int rk_device_count(int32_t* count) {
 namespace {
 // half_margin (percent): a chunk runs half-warp when its modelled cost is
 // below half_margin % of the best full-warp option; 0 builds the layout
-// without half-warp chunks (the full-warp twin, rk_bank_s::full_bank).
+// without lane-group chunks (the full-warp twin, rk_bank_s::narrow[0]);
+// max_group caps the series per pass of the lane-group kinds (1 / 2 / 4 / 8).
 int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, const int32_t* dilations,
                      const int32_t* paddings, const float* biases, const float* weights, const int64_t* woff,
                      const int32_t* chidx, const int64_t* choff, const int32_t* chcnt, int32_t device,
-                     int64_t half_margin, bool allow_quarter, rk_bank_t* out) {
+                     int64_t half_margin, int max_group, rk_bank_t* out) {
   if (!out) return fail(RK_ERR_INVALID, "bank output pointer is NULL");
   *out = nullptr;
   if (K < 1) return fail(RK_ERR_INVALID, "bank must contain at least one kernel");
@@ -1001,7 +1002,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   const int half_ctas = std::min<int>(
       std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))), cta_cap);
   const bool sp_ok = !getenv("RK_NO_SP");
-  const bool half_ok = half_margin > 0 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
+  const bool half_ok = half_margin > 0 && max_group >= 2 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   // quarter-warp chunks (8 lanes per series, four series per pass): the
   // same rule with four staged series per CTA
@@ -1009,8 +1010,12 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   // percent; default: the half-warp margin)
   const int64_t quarter_margin =
       getenv("RK_QUARTER_MARGIN") ? atoi(getenv("RK_QUARTER_MARGIN")) : half_margin;
-  const bool quarter_ok = half_ok && allow_quarter && !getenv("RK_NO_QUARTER") &&
+  const bool quarter_ok = half_ok && max_group >= 4 && !getenv("RK_NO_QUARTER") &&
                           (int64_t)half_ctas * (4 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
+  // eighth-warp chunks (4 lanes per series, eight series per pass)
+  const bool eighth_ok = quarter_ok && max_group >= 8 && !getenv("RK_NO_EIGHTH") &&
+                         (int64_t)half_ctas * (8 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
+  const int64_t eighth_margin = getenv("RK_EIGHTH_MARGIN") ? atoi(getenv("RK_EIGHTH_MARGIN")) : quarter_margin;
   std::vector<float> wpack;
   std::vector<int> chan_off;
   for (auto& kv : groups) {
@@ -1098,10 +1103,19 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
               lanes = 8;
             }
           }
+          if (eighth_ok) {
+            const int64_t c4 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 4) - fixed) / 8 + fixed;
+            if (c4 * 100 < best * eighth_margin) {
+              best = c4;
+              best_r = ri;
+              lanes = 4;
+            }
+          }
         }
       }
       if (lanes == 16) nck = nck == 0 ? 4 : 5;
       if (lanes == 8) nck = nck == 0 ? 8 : 9;
+      if (lanes == 4) nck = nck == 0 ? 10 : 11;
       hc.cost = best;
       dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
       // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is
@@ -1147,6 +1161,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       k0 += nk;
     }
   }
+  for (const auto& hc : b->chunks) b->max_groups = std::max(b->max_groups, rk::nck_groups(hc.dev.cls % rk::kNumNck));
   // RK_DUMP_CHUNKS=<path>: the chunk layout, one line per chunk (diagnostics)
   if (const char* dump = getenv("RK_DUMP_CHUNKS")) {
     if (FILE* f = fopen(dump, "a")) {
@@ -1345,24 +1360,12 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   const int64_t margin_fast = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
   const int64_t margin_exact = getenv("RK_HALF_MARGIN_EXACT") ? atoi(getenv("RK_HALF_MARGIN_EXACT")) : 110;
   int rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
-                            margin_fast, true, out);
+                            margin_fast, 8, out);
   if (rc) return rc;
   rk_bank_t b = *out;
-  auto has_half = [](rk_bank_t x) {
-    for (const auto& wl : x->wide_launches) {
-      const int k = wl.cls % rk::kNumNck;
-      if (rk::nck_half(k) || rk::nck_quarter(k)) return true;
-    }
-    return false;
-  };
-  auto has_quarter = [](rk_bank_t x) {
-    for (const auto& wl : x->wide_launches)
-      if (rk::nck_quarter(wl.cls % rk::kNumNck)) return true;
-    return false;
-  };
-  auto twin = [&](int64_t margin, rk_bank_t* dst, bool quarter = false) -> int {
+  auto impl = [&](int64_t margin, int max_group, rk_bank_t* dst) -> int {
     int r = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt,
-                             device, margin, quarter, dst);
+                             device, margin, max_group, dst);
     if (r) {
       delete b;
       *out = nullptr;
@@ -1371,26 +1374,31 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
     b->device_bytes += (*dst)->device_bytes;
     return RK_OK;
   };
-  if (has_half(b)) {
-    // Transforms whose items hold one series (few series) run the full-warp
-    // twin: half-warp chunks there would run on the full-warp kernel at an
-    // R priced for 16 lanes (config 2 bank at 2,000 series: -6 % fast,
-    // -11 % exact).
-    if ((rc = twin(0, &b->full_bank))) return rc;
-    // items of two or three series: the layout without quarter-warp chunks
-    if (has_quarter(b) && (rc = twin(margin_fast, &b->half_bank))) return rc;
-    // exact mode (FMUL2 + FFMA2 per tap) favours half-warp chunks more
-    // (quarter-warp chunks included: FordA shape exact 330k -> 354k series/s),
-    // with its own half-warp twin for items of two or three series
-    if (margin_exact != margin_fast) {
-      if ((rc = twin(margin_exact, &b->exact_bank, true))) return rc;
-      if (!has_half(b->exact_bank)) {
-        b->device_bytes -= b->exact_bank->device_bytes;
-        delete b->exact_bank;
-        b->exact_bank = nullptr;
-      } else if (has_quarter(b->exact_bank)) {
-        if ((rc = twin(margin_exact, &b->exact_bank->half_bank))) return rc;
-      }
+  // Narrower twins for items that cannot fill this layout's widest lane
+  // groups: e.g. the config-2 bank at 2,000 series (one series per item)
+  // runs the full-warp twin (-6 % fast, -11 % exact otherwise).
+  auto narrow_twins = [&](rk_bank_t x, int64_t margin, int from) -> int {
+    for (int j = from; j < 3; ++j) {
+      const int g = 1 << j;
+      if (g >= x->max_groups) break;
+      int r = impl(g == 1 ? 0 : margin, g, &x->narrow[j]);
+      if (r) return r;
+    }
+    return RK_OK;
+  };
+  if ((rc = narrow_twins(b, margin_fast, 0))) return rc;
+  // exact mode (FMUL2 + FFMA2 per tap) favours lane groups more: its own
+  // layout priced with margin_exact (FordA shape exact 330k -> 354k with
+  // quarter-warp chunks), with its own narrower twins (items of one series
+  // run the fast layout's full-warp twin, which is mode-independent)
+  if (margin_exact != margin_fast && b->max_groups > 1) {
+    if ((rc = impl(margin_exact, 8, &b->exact_bank))) return rc;
+    if (b->exact_bank->max_groups == 1) {
+      b->device_bytes -= b->exact_bank->device_bytes;
+      delete b->exact_bank;
+      b->exact_bank = nullptr;
+    } else if ((rc = narrow_twins(b->exact_bank, margin_exact, 1))) {
+      return rc;
     }
   }
   return RK_OK;
@@ -1420,6 +1428,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
   for (const auto& hc : b->chunks) {
     info->n_half_chunks += rk::nck_half(hc.dev.cls % rk::kNumNck) ? 1 : 0;
     info->n_quarter_chunks += rk::nck_quarter(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+    info->n_eighth_chunks += rk::nck_eighth(hc.dev.cls % rk::kNumNck) ? 1 : 0;
     info->n_paired_chunks += rk::nck_sp(hc.dev.cls % rk::kNumNck) ? 1 : 0;
   }
   if (b->wide_path)

@@ -79,7 +79,7 @@ __host__ __device__ constexpr int r_of(int r_idx) {
 constexpr int kExactRMax = 13;
 constexpr int kExactRIdx13 = 5;
 static_assert(r_of(kExactRIdx13) == kExactRMax, "R class table");
-constexpr int kNumNck = 10;
+constexpr int kNumNck = 12;
 // (P, NC) of a channel kind on the wide path; NC = 0: run-time slot loop.
 // 4 / 5: the 1-channel kinds 0 / 3 run as half-warp chunks (two series per
 // pass); same chunk data, so they fall back to 0 / 3 when items hold one
@@ -87,22 +87,26 @@ constexpr int kNumNck = 10;
 // position-paired ("SP"): the two FFMA2 lanes hold two positions of the
 // one kernel instead of a kernel and an idle zero-weight slot.
 // 8 / 9: the 1-channel kinds 0 / 3 as quarter-warp chunks (four series per
-// pass, 8 lanes each); they run as the half-warp kinds 4 / 5 when items
-// hold two or three series.
-__host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4 || nck == 8) ? 2 : 1; }
+// pass, 8 lanes each); 10 / 11: as eighth-warp chunks (eight series per
+// pass, 4 lanes each).  A transform whose items hold fewer series than a
+// kind's groups runs a narrower twin layout of the bank.
+__host__ __device__ constexpr int nck_pairs(int nck) { return (nck == 0 || nck == 4 || nck == 8 || nck == 10) ? 2 : 1; }
 __host__ __device__ constexpr int nck_slots(int nck) { return (nck == 1 || nck == 7) ? 2 : nck == 2 ? 0 : 1; }
 __host__ __device__ constexpr bool nck_half(int nck) { return nck == 4 || nck == 5; }
 __host__ __device__ constexpr bool nck_quarter(int nck) { return nck == 8 || nck == 9; }
+__host__ __device__ constexpr bool nck_eighth(int nck) { return nck == 10 || nck == 11; }
 __host__ __device__ constexpr bool nck_sp(int nck) { return nck == 6 || nck == 7; }
 // lanes per series group of a kind (32: the whole warp on one series)
-__host__ __device__ constexpr int nck_lanes(int nck) { return nck_half(nck) ? 16 : nck_quarter(nck) ? 8 : 32; }
-// the half-warp kind of a quarter-warp kind
-__host__ __device__ constexpr int nck_as_half(int nck) { return nck == 8 ? 4 : nck == 9 ? 5 : nck; }
+__host__ __device__ constexpr int nck_lanes(int nck) {
+  return nck_half(nck) ? 16 : nck_quarter(nck) ? 8 : nck_eighth(nck) ? 4 : 32;
+}
+// series per pass of a kind (1, 2, 4, 8)
+__host__ __device__ constexpr int nck_groups(int nck) { return 32 / nck_lanes(nck); }
 // largest R of the position-paired kinds (2R positions per lane: the pair
 // window and accumulators fit the ~80-register budget)
 __host__ __device__ constexpr int sp_rmax(int nc, int len) { return nc == 1 ? (len == 7 ? 9 : 7) : 5; }
 __host__ __device__ constexpr int nck_full(int nck) {
-  return (nck == 4 || nck == 8) ? 0 : (nck == 5 || nck == 9) ? 3 : nck;
+  return (nck == 4 || nck == 8 || nck == 10) ? 0 : (nck == 5 || nck == 9 || nck == 11) ? 3 : nck;
 }
 constexpr int kNumClasses = 3 * kNumR * kNumNck;
 
@@ -494,7 +498,7 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
                                               int r32, float invd, const float* nan_slot, int lane) {
-  constexpr int kLog = LANES == 32 ? 5 : LANES == 16 ? 4 : 3;
+  constexpr int kLog = LANES == 32 ? 5 : LANES == 16 ? 4 : LANES == 8 ? 3 : 2;
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
@@ -1550,8 +1554,9 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           // the last series shadow it and write nothing
           static_assert(!GMEM && !(MPV && EXACT), "lane-group chunks: staged series; MPV in fast mode");
           constexpr int NG = 32 / LG;
-          const int grp = lane >> (LG == 16 ? 4 : 3), hl = lane & (LG - 1);
-          const int qg = c.q32 >> (NG == 2 ? 1 : 2), rg = LG - qg * c.d;  // LG / d, LG % d
+          constexpr int kLogLG = LG == 16 ? 4 : LG == 8 ? 3 : 2;
+          const int grp = lane >> kLogLG, hl = lane & (LG - 1);
+          const int qg = c.q32 >> (5 - kLogLG), rg = LG - qg * c.d;  // LG / d, LG % d
           for (int si = 0; si < ns; si += NG) {
             const int sj = min(si + grp, ns - 1);
             const float* sx = sbase + sj * slot + H;

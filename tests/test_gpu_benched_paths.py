@@ -60,7 +60,7 @@ def test_benched_fast_path_full_size(name, n, c, l, stride, cuda_ready):
     db = device_bank(bank, 0)
     if c == 1 and l <= 2048:
         # the layout the bench runs: half-warp chunks (two series per pass)
-        assert db.info["n_half_chunks"] + db.info["n_quarter_chunks"] > 0
+        assert db.info["n_half_chunks"] + db.info["n_quarter_chunks"] + db.info["n_eighth_chunks"] > 0
     x = torch.from_numpy(values).cuda()
     rows = np.arange(0, n, stride)
     rows[-1] = n - 1

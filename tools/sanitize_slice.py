@@ -46,7 +46,7 @@ def main():
     rows = np.arange(0, n, n // 12)
     bank = generate_bank(1024, 1, 1000, GenOptions(seed=0))
     info = device_bank(bank, 0).info
-    assert info["n_half_chunks"] + info["n_quarter_chunks"] > 0
+    assert info["n_half_chunks"] + info["n_quarter_chunks"] + info["n_eighth_chunks"] > 0
     values = synth_random(n, 1, 1024, seed=1).values
     ref = oracle_transform(values[rows], bank)
     assert dev_run(bank, values, "exact")[rows].tobytes() == ref.tobytes()
