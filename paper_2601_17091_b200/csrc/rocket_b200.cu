@@ -414,15 +414,40 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
   // work; many series: wide_ctas_per_sm CTAs of 24/ctas warps.
   int ctas = b->wide_ctas_per_sm;
   if (n < 4LL * st->sms * ctas) ctas = std::min(b->wide_ctas_smem, rk::kWideMaxWarps);
-  const int warps = std::max(1, rk::kWideMaxWarps / ctas);
   // several series per item when they fit at the same CTA count: each
   // chunk's weights and setup serve all of them
   const int spi_max = getenv("RK_SPI") ? std::max(1, atoi(getenv("RK_SPI"))) : 8;
-  int spi = 1;
-  const int64_t min_items = getenv("RK_MIN_ITEMS") ? atoi(getenv("RK_MIN_ITEMS")) : 2;
-  while (spi < spi_max && n >= min_items * (spi + 1) * st->sms * ctas &&
-         (int64_t)ctas * ((spi + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
-    ++spi;
+  const int64_t min_items_env = getenv("RK_MIN_ITEMS") ? atoi(getenv("RK_MIN_ITEMS")) : 0;
+  auto spi_for = [&](int c, int64_t min_items) {
+    int v = 1;
+    while (v < spi_max && n >= min_items * (v + 1) * st->sms * c &&
+           (int64_t)c * ((v + 1) * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024)
+      ++v;
+    return v;
+  };
+  auto pass_width = [&](int v) {  // series per pass an item of v series fills in this layout
+    int w = 1;
+    while (w * 2 <= v && w * 2 <= b->max_groups) w *= 2;
+    return w;
+  };
+  int spi = spi_for(ctas, min_items_env ? min_items_env : 2);
+  // A layout with lane groups wider than the items can fill: try fewer,
+  // wider CTAs (down to 2) and one item per CTA slot, keeping the CTA count
+  // that fills the widest groups (FordA shape: 3 x 8 warps with 4-series
+  // items -> 2 x 12 with 8-series items, eighth-warp chunks: +3.4 %).
+  if (!min_items_env && b->max_groups > 1 && pass_width(spi) < b->max_groups && !getenv("RK_WIDE_CTAS")) {
+    int best_c = ctas, best_v = spi;
+    for (int c = ctas; c >= 2; --c) {
+      const int v = spi_for(c, c == ctas ? 2 : 1);
+      if (pass_width(v) > pass_width(best_v)) {
+        best_c = c;
+        best_v = v;
+      }
+    }
+    ctas = best_c;
+    spi = best_v;
+  }
+  const int warps = std::max(1, rk::kWideMaxWarps / ctas);
   // whole passes of the lane groups: no shadowed groups in the last pass of
   // an item (a 6-series item on quarter-warp chunks wasted 1/4 of a pass:
   // config 2 at 4 CTAs 240k -> 314k series/s); RK_SPI_ROUND=0 disables
