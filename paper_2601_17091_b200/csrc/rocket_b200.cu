@@ -1552,6 +1552,13 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
   const int64_t nbatch_min = getenv("RK_E2E_BATCHES") ? std::max(1, atoi(getenv("RK_E2E_BATCHES"))) : 6;
   const int64_t min_rows = getenv("RK_E2E_MIN_ROWS") ? std::max(1, atoi(getenv("RK_E2E_MIN_ROWS"))) : 4096;
   if (n >= min_rows) batch = std::min<int64_t>(batch, (n + nbatch_min - 1) / nbatch_min);
+  // Few rows: up to three equal batches of >= 1,000 rows, so the features of
+  // one batch copy out while the next computes (FordA shape, 3,601 rows: one
+  // batch 311k -> three 413k series/s end to end; smaller batches turn
+  // launch-bound: 8 batches 164k).
+  else if (!getenv("RK_E2E_BATCHES"))
+    batch = std::min<int64_t>(batch, (n + std::max<int64_t>(1, std::min<int64_t>(3, n / 1000)) - 1) /
+                                         std::max<int64_t>(1, std::min<int64_t>(3, n / 1000)));
   // Batch schedule: the features of a batch are complete only when its whole
   // launch chain has run, so the last batch's D2H is exposed after the last
   // kernel.  Batches shrink geometrically towards the end (tail rows, x2
