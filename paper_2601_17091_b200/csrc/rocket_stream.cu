@@ -318,6 +318,12 @@ int run_stream(rk_bank_t bank, const StreamIO& io, int64_t n, int32_t dtype, int
     batch = std::min<int64_t>(batch, 65535);
     // long series: bound the pinned input slots too
     batch = std::min<int64_t>(batch, std::max<int64_t>(64, ((int64_t)512 << 20) / std::max<int64_t>(1, dev_row)));
+    // a few thousand rows: up to three batches of >= 1,000 rows so copies
+    // overlap the kernels (as rk_transform's pinned pipeline)
+    if (n < batch) {
+      const int64_t k = std::max<int64_t>(1, std::min<int64_t>(3, n / 1000));
+      batch = (n + k - 1) / k;
+    }
   }
   batch = std::min(batch, n);
   const int64_t nb = (n + batch - 1) / batch;
