@@ -16,3 +16,19 @@ int rk_stream_counter(rk_bank_t bank, void* stream, unsigned long long** counter
 int rk_stream_host(rk_bank_t bank, const void* x, int32_t dtype, int64_t n, void* out, int64_t ld_out, int64_t row0,
                    int32_t fpk, int32_t mode, int64_t* executed);
 }
+
+// NVTX ranges (SURVEY §5 tracing): visible in Nsight Systems / ncu range
+// filters, near-zero cost without a tool attached (header-only nvtx3).
+#include <nvtx3/nvToolsExt.h>
+#include <cstdio>
+struct RkRange {
+  explicit RkRange(const char* name) { nvtxRangePushA(name); }
+  RkRange(const char* fmt, long long a, long long b) {
+    char buf[96];
+    std::snprintf(buf, sizeof(buf), fmt, a, b);
+    nvtxRangePushA(buf);
+  }
+  ~RkRange() { nvtxRangePop(); }
+  RkRange(const RkRange&) = delete;
+  RkRange& operator=(const RkRange&) = delete;
+};

@@ -473,6 +473,7 @@ int launch_wide_chain(rk_bank_t b, DeviceState* st, const float* d_x, int64_t n,
                                nanp);
   }
   const int64_t grid = std::min<int64_t>((n + spi - 1) / spi, (int64_t)st->sms * ctas);
+  RkRange range("rk launch chain spi=%lld launches=%lld", (long long)spi, (long long)b->wide_launches.size());
   if (profile)
     fprintf(stderr, "RK_PROFILE chain n=%lld spi=%d ctas=%d warps=%d launches=%zu max_groups=%d exact_twin=%d\n",
             (long long)n, spi, ctas, warps, b->wide_launches.size(), b->max_groups, b->exact_bank != nullptr);
@@ -1465,6 +1466,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
 
 int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* outv, int64_t ld_out, int64_t row0,
                  int32_t fpk, int32_t mode, void* stream_ptr, int64_t* executed) {
+  RkRange range("rk_transform n=%lld mode=%lld", (long long)n, (long long)mode);
   if (!b) return fail(RK_ERR_INVALID, "NULL bank");
   if (n < 0 || row0 < 0) return fail(RK_ERR_INVALID, "n_series and row0 must be non-negative");
   if (fpk != 2 && fpk != 3) return fail(RK_ERR_INVALID, "features_per_kernel=%d must be 2 or 3", fpk);
@@ -1619,6 +1621,7 @@ int rk_transform(rk_bank_t b, const void* xv, int32_t dtype, int64_t n, void* ou
   for (int64_t k = 0; k < nbatch; ++k) {
     const int64_t s0 = starts[k], cnt = sizes[k];
     const int ib = (int)(k % kInBufs), ob = (int)(k % kOutBufs);
+    RkRange brange("rk pinned batch %lld rows=%lld", (long long)k, (long long)cnt);
     if (!dx && k + 1 < nbatch) {
       rc = h2d(k + 1);  // enqueued before this batch's D2H
       if (rc) return rc;

@@ -298,6 +298,7 @@ struct StreamIO {
 
 int run_stream(rk_bank_t bank, const StreamIO& io, int64_t n, int32_t dtype, int32_t fpk, int32_t mode,
                int64_t batch_rows, int64_t* executed) {
+  RkRange range("rk stream n=%lld mode=%lld", (long long)n, (long long)mode);
   rk_bank_info_t info;
   int rc = rk_bank_info(bank, &info);
   if (rc) return rc;
