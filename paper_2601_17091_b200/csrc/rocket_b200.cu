@@ -58,7 +58,8 @@ constexpr int kLenIdx[12] = {-1, -1, -1, -1, -1, -1, -1, 0, -1, 1, -1, 2};
 
 struct HostChunk {
   rk::DevChunk dev;
-  int64_t cost;  // instruction-slot estimate for one series
+  int64_t cost;       // instruction-slot estimate for one series
+  bool tail = false;  // tail mode (the wide kernel's WChunk flag)
 };
 
 // Instruction-slot estimate of one chunk for one series at a given R
@@ -67,13 +68,15 @@ struct HostChunk {
 // masked steps for the leftover positions.
 // lanes = 16: half-warp chunks, whose steps serve two series (the caller
 // halves the step part).
-int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false, int lanes = 32) {
+int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false, int lanes = 32, bool tail = false) {
   const int64_t G = 2 * P;
   const int64_t RD = (int64_t)R * d;
   const int64_t A = n / RD;
   const int64_t rem = n - A * RD;
   const int64_t full_starts = A * d;
-  const int64_t starts = full_starts + std::min<int64_t>(d, rem);
+  // tail mode: the R map covers the complete runs only and the remaining
+  // rem positions run as an R = 1 map (no partial runs)
+  const int64_t starts = tail ? full_starts : full_starts + std::min<int64_t>(d, rem);
   const int64_t nfull = full_starts / lanes;
   const int64_t masked_steps = (starts - nfull * lanes + lanes - 1) / lanes;
   auto step = [&](int64_t r, int64_t extra) {
@@ -88,29 +91,42 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false
   // NaN-slot masking, transform_kernel.cuh load_window_masked)
   static const int mpct = getenv("RK_MASK_COST_PCT") ? atoi(getenv("RK_MASK_COST_PCT")) : 100;
   static const int chunk_extra = getenv("RK_CHUNK_COST") ? atoi(getenv("RK_CHUNK_COST")) : 60;
-  return nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) * mpct / 100 + 40 * G + chunk_extra;
+  int64_t c = nfull * step(R, 8) + masked_steps * (step(R, 18) + 4 * R * nc) * mpct / 100 + 40 * G + chunk_extra;
+  if (tail && rem > 0) {
+    const int64_t tf = rem / lanes, tm = (rem - tf * lanes + lanes - 1) / lanes;
+    c += tf * step(1, 8) + tm * (step(1, 18) + 4 * nc) * mpct / 100;
+  }
+  return c;
 }
 
 // Cost of a position-paired single-kernel chunk (kinds 6 / 7): runs of 2R
 // positions per lane, R FFMA2 pairs per tap and slot, two window loads per
 // pair slot.
-int64_t chunk_cost_sp(int len, int d, int n, int nc, int R) {
+int64_t chunk_cost_sp(int len, int d, int n, int nc, int R, bool tail = false) {
   const int64_t RD = 2LL * R * d;
   const int64_t A = n / RD;
   const int64_t rem = n - A * RD;
   const int64_t full_starts = A * d;
-  const int64_t starts = full_starts + std::min<int64_t>(d, rem);
+  const int64_t starts = tail ? full_starts : full_starts + std::min<int64_t>(d, rem);
   const int64_t nfull = full_starts / 32;
   const int64_t masked_steps = (starts - nfull * 32 + 31) / 32;
-  auto step = [&](int64_t extra) {
-    return (int64_t)R * len * nc      // FFMA2
-           + 2LL * R * 2              // count (2R outputs)
-           + R                        // max (FMNMX3 pairs)
-           + 4LL * (R + len - 1) * nc  // two window loads + addresses per pair slot
+  auto step = [&](int64_t r, int64_t extra) {
+    return r * len * nc              // FFMA2
+           + 2 * r * 2               // count (2r outputs)
+           + r                       // max (FMNMX3 pairs)
+           + 4 * (r + len - 1) * nc  // two window loads + addresses per pair slot
            + extra;
   };
   static const int chunk_extra = getenv("RK_CHUNK_COST") ? atoi(getenv("RK_CHUNK_COST")) : 60;
-  return nfull * step(8) + masked_steps * (step(18) + 8LL * R * nc) + 40 * 2 + chunk_extra;
+  int64_t c = nfull * step(R, 8) + masked_steps * (step(R, 18) + 8LL * R * nc) + 40 * 2 + chunk_extra;
+  if (tail && rem > 0) {
+    // the remaining positions as an R = 1 position-paired map (runs of 2)
+    const int64_t A1 = rem / (2LL * d), rem1 = rem - A1 * 2 * d;
+    const int64_t st1 = A1 * d + std::min<int64_t>(d, rem1);
+    const int64_t f1 = (A1 * d) / 32, m1 = (st1 - f1 * 32 + 31) / 32;
+    c += f1 * step(1, 8) + m1 * (step(1, 18) + 8LL * nc);
+  }
+  return c;
 }
 
 }  // namespace
@@ -1028,6 +1044,10 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   const int half_ctas = std::min<int>(
       std::min<int>(rk::kWideMaxWarps, (int)((st->smem_optin + 1024) / (smem + 1024))), cta_cap);
   const bool sp_ok = !getenv("RK_NO_SP");
+  // tail mode (chunks with fixed channel slots on the wide path): the cost
+  // model may end a chunk's R-position runs at the last complete run and
+  // walk the remaining positions one per lane instead of as partial runs
+  const bool tail_ok = wide_ok && !gmem && !getenv("RK_NO_TAIL");
   const bool half_ok = half_margin > 0 && max_group >= 2 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   // quarter-warp chunks (8 lanes per series, four series per pass): the
@@ -1091,50 +1111,64 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       dc.invd = 1.0f / (float)d;
       int best_r = 0;
       int64_t best = INT64_MAX;
-      int lanes = 32;  // 16: half-warp, 8: quarter-warp chunk
+      int lanes = 32;     // 16: half-warp, 8: quarter-warp, 4: eighth-warp chunk
+      bool tail = false;  // complete runs at R, the remaining positions as an R = 1 map
       for (int ri = rk::kNumR - 1; ri >= 0; --ri) {
         if (sp) {
           if (rk::r_of(ri) > rk::sp_rmax(nc, len)) continue;
-          const int64_t cst = chunk_cost_sp(len, d, n, nc, rk::r_of(ri));
-          if (cst < best) {
-            best = cst;
-            best_r = ri;
+          for (int tl = 0; tl < (tail_ok ? 2 : 1); ++tl) {
+            const int64_t cst = chunk_cost_sp(len, d, n, nc, rk::r_of(ri), tl == 1);
+            if (cst < best) {
+              best = cst;
+              best_r = ri;
+              tail = tl == 1;
+            }
           }
           continue;
         }
         if (nck == 2 && !wide_ok && ri != 0) continue;  // class-kernel generic path: 1 position per lane
         if (gmem && nck == 0 && ri > 2) continue;  // GMEM slot-loop kernels with 2 pairs: R <= 5 (registers)
-        const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), gmem || rk::nck_slots(nck) == 0);
-        if (cst < best) {
-          best = cst;
-          best_r = ri;
-          lanes = 32;
+        const bool fixed_slots = !gmem && rk::nck_slots(nck) != 0;
+        for (int tl = 0; tl < (tail_ok && fixed_slots ? 2 : 1); ++tl) {
+          const int64_t cst = chunk_cost(len, d, n, nc, P, rk::r_of(ri), !fixed_slots, 32, tl == 1);
+          if (cst < best) {
+            best = cst;
+            best_r = ri;
+            lanes = 32;
+            tail = tl == 1;
+          }
         }
         // single-channel chunks may run as half-warp chunks (two series per
         // pass of 16-lane steps: per series, half the 16-lane step cost) or
         // quarter-warp chunks (four series per pass of 8-lane steps)
         if (half_ok && nc == 1) {
           const int64_t fixed = 40 * 2 * P + 60;
-          const int64_t c16 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 16) - fixed) / 2 + fixed;
-          if (c16 * 100 < best * half_margin) {
-            best = c16;
-            best_r = ri;
-            lanes = 16;
-          }
-          if (quarter_ok) {
-            const int64_t c8 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 8) - fixed) / 4 + fixed;
-            if (c8 * 100 < best * quarter_margin) {
-              best = c8;
+          for (int tl = 0; tl < (tail_ok ? 2 : 1); ++tl) {
+            const bool t = tl == 1;
+            const int64_t c16 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 16, t) - fixed) / 2 + fixed;
+            if (c16 * 100 < best * half_margin) {
+              best = c16;
               best_r = ri;
-              lanes = 8;
+              lanes = 16;
+              tail = t;
             }
-          }
-          if (eighth_ok) {
-            const int64_t c4 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 4) - fixed) / 8 + fixed;
-            if (c4 * 100 < best * eighth_margin) {
-              best = c4;
-              best_r = ri;
-              lanes = 4;
+            if (quarter_ok) {
+              const int64_t c8 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 8, t) - fixed) / 4 + fixed;
+              if (c8 * 100 < best * quarter_margin) {
+                best = c8;
+                best_r = ri;
+                lanes = 8;
+                tail = t;
+              }
+            }
+            if (eighth_ok) {
+              const int64_t c4 = (chunk_cost(len, d, n, nc, P, rk::r_of(ri), false, 4, t) - fixed) / 8 + fixed;
+              if (c4 * 100 < best * eighth_margin) {
+                best = c4;
+                best_r = ri;
+                lanes = 4;
+                tail = t;
+              }
             }
           }
         }
@@ -1143,6 +1177,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       if (lanes == 8) nck = nck == 0 ? 8 : 9;
       if (lanes == 4) nck = nck == 0 ? 10 : 11;
       hc.cost = best;
+      hc.tail = tail;
       dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
       // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is
       // centred in the LEN-tap frame with zero taps at both ends.
@@ -1283,7 +1318,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
               wc.ch[1] = c.nc;
             }
             wc.q32 = (short)c.q32;
-            wc.r32 = (short)c.r32;
+            wc.r32 = (short)(c.r32 | (b->chunks[i0 + j].tail ? rk::kTailFlag : 0));
             wc.invd = c.invd;
             std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
             std::memcpy(raw + cursor, wpack.data() + c.wofs, wbytes);

@@ -497,13 +497,16 @@ template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, int LANES
 __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
-                                              int r32, float invd, const float* nan_slot, int lane) {
+                                              int r32, float invd, const float* nan_slot, int lane,
+                                              bool tail = false) {
   constexpr int kLog = LANES == 32 ? 5 : LANES == 16 ? 4 : LANES == 8 ? 3 : 2;
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
   const int rem = n - A * RD;    // positions of the partial run
   const int full_starts = A * d;
-  const int starts = full_starts + min(d, rem);
+  // tail mode: stop at the last complete run; the rem positions [A*R*d, n)
+  // — a contiguous range — run below as an R = 1 map
+  const int starts = (R > 1 && tail) ? full_starts : full_starts + min(d, rem);
   const int nfull = full_starts >> kLog;
   // (a, s) = divmod(32*step + lane, d), advanced incrementally; the first
   // divmod of lane < 32 is exact in float ((lane + 0.5) / d is never within
@@ -532,6 +535,11 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
       s -= d;
       v0 += RD - d;
     }
+  }
+  if constexpr (R > 1) {
+    if (tail && rem > 0)
+      run_positions<LEN, 1, P, NC, EXACT, MPV, LANES>(st, chan, w, thr, init, one2, lo + A * RD, rem, d, q32, r32,
+                                                      invd, nan_slot, lane, false);
   }
 }
 
@@ -595,12 +603,12 @@ template <int LEN, int R, int NC, bool EXACT, bool MPV = false>
 __device__ __forceinline__ void run_positions_sp(Pool<2, MPV>& st, const float* const (&chan)[NC],
                                                  const float (&w)[NC][LEN], const float (&thr)[2], float2 init,
                                                  float2 one2, int lo, int n, int d, int q32, int r32, float invd,
-                                                 const float* nan_slot, int lane) {
+                                                 const float* nan_slot, int lane, bool tail = false) {
   const int RD = 2 * R * d;
   const int A = n / RD;
   const int rem = n - A * RD;
   const int full_starts = A * d;
-  const int starts = full_starts + min(d, rem);
+  const int starts = (R > 1 && tail) ? full_starts : full_starts + min(d, rem);  // see run_positions
   const int nfull = full_starts >> 5;
   int a = (int)((lane + 0.5f) * invd);
   int s = lane - a * d;
@@ -626,6 +634,11 @@ __device__ __forceinline__ void run_positions_sp(Pool<2, MPV>& st, const float* 
       s -= d;
       v0 += RD - d;
     }
+  }
+  if constexpr (R > 1) {
+    if (tail && rem > 0)
+      run_positions_sp<LEN, 1, NC, EXACT, MPV>(st, chan, w, thr, init, one2, lo + A * RD, rem, d, q32, r32, invd,
+                                               nan_slot, lane, false);
   }
 }
 
@@ -928,6 +941,11 @@ struct float4_t {  // host-side storage of the parameter blob
   float x, y, z, w;
 };
 
+// WChunk.r32 bit 14: tail mode (complete runs at R, the remaining positions
+// as an R = 1 map); the low bits hold 32 % d.  The fast-MPV kernels ignore
+// the flag (their partial sums leave no registers for the R = 1 path) and
+// walk those chunks as partial runs: the same outputs in another order.
+constexpr short kTailFlag = 0x4000;
 struct __align__(16) WChunk {  // 80 bytes
   int d, lo, n, nk;
   int col[4];
@@ -1533,8 +1551,9 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
             Pool<2, MPV> st;
             pool_init<2, EXACT, MPV>(st);
-            run_positions_sp<LEN, R, NC, EXACT, MPV>(st, chan, ws, thr2, init2, one2, c.lo, c.n, c.d, c.q32, c.r32,
-                                                     c.invd, nanp, lane);
+            run_positions_sp<LEN, R, NC, EXACT, MPV>(st, chan, ws, thr2, init2, one2, c.lo, c.n, c.d, c.q32,
+                                                     c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
+                                                     !MPV && (c.r32 & kTailFlag) != 0);
             finish_chunk_sp<EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out,
                                                 lane);
             done += (unsigned long long)c.n;
@@ -1566,7 +1585,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             Pool<2 * P, MPV> st;
             pool_init<2 * P, EXACT, MPV>(st);
             run_positions<LEN, R, P, NC, EXACT, MPV, LG>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, qg, rg,
-                                                         c.invd, nanp, hl);
+                                                         c.invd, nanp, hl, !MPV && (c.r32 & kTailFlag) != 0);
             float* orow0 = p.h.out + (series0 + si) * p.h.ld_out;
             float* orow = orow0;
 #pragma unroll
@@ -1585,8 +1604,9 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           for (int s = 0; s < NC; ++s) chan[s] = sx + c.ch[s] * S;
           Pool<2 * P, MPV> st;
           pool_init<2 * P, EXACT, MPV>(st);
-          run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32, c.r32,
-                                                   c.invd, nanp, lane);
+          run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32,
+                                                   c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
+                                                   !MPV && (c.r32 & kTailFlag) != 0);
           finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
                                                   p.h.vec_out, lane);
           done += (unsigned long long)c.nk * (unsigned long long)c.n;
