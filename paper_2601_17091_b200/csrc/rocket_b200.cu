@@ -1229,9 +1229,9 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       fprintf(f, "# bank K=%lld C=%d L=%d half_margin=%lld\n", (long long)K, C, L, (long long)half_margin);
       for (const auto& hc : b->chunks) {
         const rk::DevChunk& c = hc.dev;
-        fprintf(f, "len=%d R=%d nck=%d d=%d lo=%d n=%d nk=%d nc=%d cost=%lld\n", c.len,
+        fprintf(f, "len=%d R=%d nck=%d d=%d lo=%d n=%d nk=%d nc=%d cost=%lld tail=%d\n", c.len,
                 rk::r_of((c.cls / rk::kNumNck) % rk::kNumR), c.cls % rk::kNumNck, c.d, c.lo, c.n, c.nk, c.nc,
-                (long long)hc.cost);
+                (long long)hc.cost, hc.tail ? 1 : 0);
       }
       fclose(f);
     }
