@@ -99,17 +99,17 @@ int64_t chunk_cost(int len, int d, int n, int nc, int P, int R, bool dyn = false
   return c;
 }
 
-// Cost of a position-paired single-kernel chunk (kinds 6 / 7): runs of 2R
-// positions per lane, R FFMA2 pairs per tap and slot, two window loads per
-// pair slot.
+// Cost of a position-paired single-kernel chunk (kinds 6 / 7): two runs of R
+// positions per lane (64 run starts per step), R FFMA2 pairs per tap and
+// slot, two window loads per pair slot.
 int64_t chunk_cost_sp(int len, int d, int n, int nc, int R, bool tail = false) {
-  const int64_t RD = 2LL * R * d;
-  const int64_t A = n / RD;
-  const int64_t rem = n - A * RD;
-  const int64_t full_starts = A * d;
-  const int64_t starts = tail ? full_starts : full_starts + std::min<int64_t>(d, rem);
-  const int64_t nfull = full_starts / 32;
-  const int64_t masked_steps = (starts - nfull * 32 + 31) / 32;
+  auto steps = [&](int64_t nn, int64_t r, bool tl, int64_t& nfull, int64_t& masked) {
+    const int64_t RD = r * d, A = nn / RD, rem = nn - A * RD, full_starts = A * d;
+    const int64_t starts = tl ? full_starts : full_starts + std::min<int64_t>(d, rem);
+    nfull = full_starts / 64;
+    masked = (starts - nfull * 64 + 63) / 64;
+    return rem;
+  };
   auto step = [&](int64_t r, int64_t extra) {
     return r * len * nc              // FFMA2
            + 2 * r * 2               // count (2r outputs)
@@ -118,12 +118,12 @@ int64_t chunk_cost_sp(int len, int d, int n, int nc, int R, bool tail = false) {
            + extra;
   };
   static const int chunk_extra = getenv("RK_CHUNK_COST") ? atoi(getenv("RK_CHUNK_COST")) : 60;
-  int64_t c = nfull * step(R, 8) + masked_steps * (step(R, 18) + 8LL * R * nc) + 40 * 2 + chunk_extra;
-  if (tail && rem > 0) {
-    // the remaining positions as an R = 1 position-paired map (runs of 2)
-    const int64_t A1 = rem / (2LL * d), rem1 = rem - A1 * 2 * d;
-    const int64_t st1 = A1 * d + std::min<int64_t>(d, rem1);
-    const int64_t f1 = (A1 * d) / 32, m1 = (st1 - f1 * 32 + 31) / 32;
+  int64_t nf = 0, nm = 0;
+  const int64_t rem = steps(n, R, tail && R > 1, nf, nm);
+  int64_t c = nf * step(R, 8) + nm * (step(R, 18) + 8LL * R * nc) + 40 * 2 + chunk_extra;
+  if (tail && R > 1 && rem > 0) {
+    int64_t f1 = 0, m1 = 0;
+    steps(rem, 1, false, f1, m1);
     c += f1 * step(1, 8) + m1 * (step(1, 18) + 8LL * nc);
   }
   return c;

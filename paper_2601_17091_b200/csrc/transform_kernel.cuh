@@ -543,16 +543,17 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
   }
 }
 
-// Position-paired step (single-kernel chunks, kinds 6 / 7): a lane's run
-// holds 2R positions u0 + m*d (m < 2R); FFMA2 lane .x computes position r,
-// lane .y position r + R, both with the one kernel's weight (w, w) and the
-// series values (x[r + j], x[r + R + j]) — a kernel slot that would idle
-// beside a zero-weight partner does useful work instead.  Window element e
-// is loaded into pair slot e (.x) and pair slot e - R (.y); the masking
-// follows load_window_masked element by element (a dead position's last
-// tap reads the canonical NaN).  Per output the arithmetic is the one of
-// chunk_step: same taps, same order, same rounding.
-template <int LEN, int R>
+// Position-paired step (single-kernel chunks, kinds 6 / 7): a lane holds two
+// runs of R positions, run A at u0a + m*d and run B at u0b + m*d (m < R);
+// FFMA2 lane .x computes run A's position r, lane .y run B's, both with the
+// one kernel's weight (w, w) and the series values (xa[r + j], xb[r + j]) —
+// a kernel slot that would idle beside a zero-weight partner does useful
+// work instead.  The two windows are disjoint, so every element is loaded
+// once, straight into its half of a pair slot.  Masking follows
+// load_window_masked per run (a dead position's last tap reads the
+// canonical NaN).  Per output the arithmetic is the one of chunk_step: same
+// taps, same order, same rounding.
+template <int LEN>
 __device__ __forceinline__ float sp_load(const float* p, int e, int d, int nleft, const float* nan_slot, bool masked) {
   const float* a = p + e * d;
   if (masked && e >= LEN - 1) a = (e - (LEN - 1)) * d < nleft ? a : nan_slot;
@@ -563,24 +564,26 @@ __device__ __forceinline__ float sp_load(const float* p, int e, int d, int nleft
 template <int LEN, int R, int NC, bool EXACT, bool MASKED, bool MPV = false>
 __device__ __forceinline__ void chunk_step_sp(Pool<2, MPV>& st, const float* const (&chan)[NC],
                                               const float (&w)[NC][LEN], const float (&thr)[2], float2 init,
-                                              float2 one2, int u0, int d, int nleft, const float* nan_slot) {
+                                              float2 one2, int u0a, int u0b, int d, int nlefta, int nleftb,
+                                              const float* nan_slot) {
   constexpr int C = (LEN - 1) / 2;
   constexpr int W = R + LEN - 1;
   float2 acc[1][R];
 #pragma unroll
   for (int s = 0; s < NC; ++s) {
-    const float* p = chan[s] + (u0 - C * d);
+    const float* pa = chan[s] + (u0a - C * d);
+    const float* pb = chan[s] + (u0b - C * d);
     float2 xp[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) {
-      xp[q].x = sp_load<LEN, R>(p, q, d, nleft, nan_slot, MASKED);
-      xp[q].y = sp_load<LEN, R>(p, q + R, d, nleft, nan_slot, MASKED);
+      xp[q].x = sp_load<LEN>(pa, q, d, nlefta, nan_slot, MASKED);
+      xp[q].y = sp_load<LEN>(pb, q, d, nleftb, nan_slot, MASKED);
     }
 #pragma unroll
     for (int j = 0; j < LEN; ++j) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        // the weight as a broadcast scalar (one uniform register)
+        // the weight as a broadcast scalar
         const float2 w2 = make_float2(w[s][j], w[s][j]);
         if (EXACT) {
           if (s == 0 && j == 0)
@@ -593,47 +596,55 @@ __device__ __forceinline__ void chunk_step_sp(Pool<2, MPV>& st, const float* con
       }
     }
   }
-  // slot 0 pools positions r, slot 1 positions r + R (same kernel)
+  // slot 0 pools run A's positions, slot 1 run B's (same kernel)
   pool_update<R, 1, EXACT, false, MPV>(st, acc, thr, true, 0, d);
 }
 
 // run_positions for position-paired chunks: the lane map of run_positions
-// with runs of 2R positions.
+// with 64 run starts per step (starts base + lane and base + 32 + lane go
+// to one lane's runs A and B).
 template <int LEN, int R, int NC, bool EXACT, bool MPV = false>
 __device__ __forceinline__ void run_positions_sp(Pool<2, MPV>& st, const float* const (&chan)[NC],
                                                  const float (&w)[NC][LEN], const float (&thr)[2], float2 init,
                                                  float2 one2, int lo, int n, int d, int q32, int r32, float invd,
                                                  const float* nan_slot, int lane, bool tail = false) {
-  const int RD = 2 * R * d;
+  const int RD = R * d;
   const int A = n / RD;
   const int rem = n - A * RD;
   const int full_starts = A * d;
   const int starts = (R > 1 && tail) ? full_starts : full_starts + min(d, rem);  // see run_positions
-  const int nfull = full_starts >> 5;
+  const int nfull = full_starts >> 6;
   int a = (int)((lane + 0.5f) * invd);
   int s = lane - a * d;
   int v0 = a * RD + s;
   const int dv = q32 * RD + r32;
+  // advance a start by 32 (the existing incremental divmod)
+  auto adv = [&](int& sv, int& vv) {
+    sv += r32;
+    vv += dv;
+    if (sv >= d) {
+      sv -= d;
+      vv += RD - d;
+    }
+  };
 #pragma unroll(kStepUnroll)
   for (int stp = 0; stp < nfull; ++stp) {
-    chunk_step_sp<LEN, R, NC, EXACT, false, MPV>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
-    s += r32;
-    v0 += dv;
-    if (s >= d) {
-      s -= d;
-      v0 += RD - d;
-    }
+    int sb = s, vb = v0;
+    adv(sb, vb);
+    chunk_step_sp<LEN, R, NC, EXACT, false, MPV>(st, chan, w, thr, init, one2, lo + v0, lo + vb, d, n, n, nan_slot);
+    s = sb;
+    v0 = vb;
+    adv(s, v0);
   }
-  for (int base = nfull << 5; base < starts; base += 32) {
-    const bool live = base + lane < starts;
-    chunk_step_sp<LEN, R, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
-                                                live ? n - v0 : 0, nan_slot);
-    s += r32;
-    v0 += dv;
-    if (s >= d) {
-      s -= d;
-      v0 += RD - d;
-    }
+  for (int base = nfull << 6; base < starts; base += 64) {
+    int sb = s, vb = v0;
+    adv(sb, vb);
+    const bool la = base + lane < starts, lb = base + 32 + lane < starts;
+    chunk_step_sp<LEN, R, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (la ? v0 : 0), lo + (lb ? vb : 0),
+                                                d, la ? n - v0 : 0, lb ? n - vb : 0, nan_slot);
+    s = sb;
+    v0 = vb;
+    adv(s, v0);
   }
   if constexpr (R > 1) {
     if (tail && rem > 0)
