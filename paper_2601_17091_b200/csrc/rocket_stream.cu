@@ -20,6 +20,7 @@
 #include "rk_internal.h"
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -543,6 +544,16 @@ extern "C" int rk_stream_host(rk_bank_t bank, const void* x, int32_t dtype, int6
   io.check_finite = false;  // the caller validated (engine._check_shapes)
   io.out = static_cast<char*>(out) + row0 * ld_out * esz;
   io.out_ld_bytes = ld_out * esz;
+  // A fresh output array (numpy's np.empty: untouched pages) is first
+  // touched by the copy threads; ask for transparent huge pages so 8 GB of
+  // features fault in 2 MB at a time instead of 4 KB (THP "madvise" mode;
+  // a no-op for pages already present or where THP is off).
+  {
+    const uintptr_t huge = (uintptr_t)2 << 20;
+    const uintptr_t beg = ((uintptr_t)io.out + huge - 1) & ~(huge - 1);
+    const uintptr_t end = ((uintptr_t)io.out + (uintptr_t)(n * ld_out * esz)) & ~(huge - 1);
+    if (end > beg) madvise((void*)beg, end - beg, MADV_HUGEPAGE);
+  }
   const unsigned hw = std::thread::hardware_concurrency();
   io.copy_threads = (int)std::max(1u, std::min(16u, hw ? hw : 4u));
   if (getenv("RK_COPY_THREADS")) io.copy_threads = std::max(1, atoi(getenv("RK_COPY_THREADS")));
