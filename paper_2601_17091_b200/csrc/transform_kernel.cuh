@@ -953,9 +953,9 @@ struct float4_t {  // host-side storage of the parameter blob
 };
 
 // WChunk.r32 bit 14: tail mode (complete runs at R, the remaining positions
-// as an R = 1 map); the low bits hold 32 % d.  The fast-MPV kernels ignore
-// the flag (their partial sums leave no registers for the R = 1 path) and
-// walk those chunks as partial runs: the same outputs in another order.
+// as an R = 1 map); the low bits hold 32 % d.  Kernels without the
+// registers for the R = 1 path (kTailOK) ignore the flag and walk those
+// chunks as partial runs: the same outputs in another order.
 constexpr short kTailFlag = 0x4000;
 struct __align__(16) WChunk {  // 80 bytes
   int d, lo, n, nk;
@@ -1480,6 +1480,10 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
   // (L1 / L2 resident) instead of a staged copy
   const float* nanp = GMEM ? p.h.nanp : &s_nan;
   const WChunk* chunks = reinterpret_cast<const WChunk*>(p.blob);
+  // tail mode support (see kTailFlag): the fast-MPV lane-group kernels at
+  // R >= 11 keep too many partial sums live for the R = 1 path and walk tail
+  // chunks as partial runs instead (the same outputs in another order)
+  constexpr bool kTailOK = !MPV || LG == 32 || R <= 9;
   const char* wbase = reinterpret_cast<const char*>(p.blob) + (size_t)p.h.n_chunks * sizeof(WChunk);
   const float2 one2 = make_float2(p.h.one, p.h.one);
   unsigned long long done = 0;
@@ -1564,7 +1568,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             pool_init<2, EXACT, MPV>(st);
             run_positions_sp<LEN, R, NC, EXACT, MPV>(st, chan, ws, thr2, init2, one2, c.lo, c.n, c.d, c.q32,
                                                      c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
-                                                     !MPV && (c.r32 & kTailFlag) != 0);
+                                                     kTailOK && (c.r32 & kTailFlag) != 0);
             finish_chunk_sp<EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out,
                                                 lane);
             done += (unsigned long long)c.n;
@@ -1596,7 +1600,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             Pool<2 * P, MPV> st;
             pool_init<2 * P, EXACT, MPV>(st);
             run_positions<LEN, R, P, NC, EXACT, MPV, LG>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, qg, rg,
-                                                         c.invd, nanp, hl, !MPV && (c.r32 & kTailFlag) != 0);
+                                                         c.invd, nanp, hl, kTailOK && (c.r32 & kTailFlag) != 0);
             float* orow0 = p.h.out + (series0 + si) * p.h.ld_out;
             float* orow = orow0;
 #pragma unroll
@@ -1617,7 +1621,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           pool_init<2 * P, EXACT, MPV>(st);
           run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32,
                                                    c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
-                                                   !MPV && (c.r32 & kTailFlag) != 0);
+                                                   kTailOK && (c.r32 & kTailFlag) != 0);
           finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
                                                   p.h.vec_out, lane);
           done += (unsigned long long)c.nk * (unsigned long long)c.n;
