@@ -996,8 +996,8 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       break;
     }
   if (getenv("RK_SSTRIDE_PAD")) spad = std::max(4, atoi(getenv("RK_SSTRIDE_PAD")) / 4 * 4);
-  const int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + spad;
-  const int64_t smem = (int64_t)C * sstride * 4;
+  int64_t sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + spad;
+  int64_t smem = (int64_t)C * sstride * 4;
   // A series that does not fit in shared memory is read from zero-haloed
   // rows in global memory instead (L1 / L2 resident; the wide kernel's
   // GMEM variants, run-time slot layout for every chunk).
@@ -1223,6 +1223,44 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
     }
   }
   for (const auto& hc : b->chunks) b->max_groups = std::max(b->max_groups, rk::nck_groups(hc.dev.cls % rk::kNumNck));
+  // Row pad by the lane-group mix: consecutive staged series sit C*e banks
+  // apart and a group of LG lanes reads LG consecutive banks, so pick the
+  // pad e whose group offsets overlap least, weighted by the modelled cost
+  // of each group width (eighth-warp chunks want 4 banks, quarter 8, half 16;
+  // at e = 16 eight 4-lane groups met in two bank ranges: 4-way replays).
+  if (!getenv("RK_SSTRIDE_PAD") && b->max_groups > 1 && !gmem) {
+    int64_t wcost[4] = {0, 0, 0, 0};  // by log2(groups): 1, 2, 4, 8
+    for (const auto& hc : b->chunks) {
+      const int g = rk::nck_groups(hc.dev.cls % rk::kNumNck);
+      wcost[g == 8 ? 3 : g == 4 ? 2 : g == 2 ? 1 : 0] += hc.cost;
+    }
+    int best_e = spad;
+    double best_score = 1e300;
+    for (int e = 4; e < 32; e += 4) {
+      double score = (double)wcost[0];
+      for (int j = 1; j < 4; ++j) {
+        const int groups = 1 << j, lg = 32 / groups;
+        int cover[32] = {};
+        for (int g = 0; g < groups; ++g)
+          for (int l = 0; l < lg; ++l) ++cover[(g * C * e + l) % 32];
+        int mult = 1;
+        for (int k2 = 0; k2 < 32; ++k2) mult = std::max(mult, cover[k2]);
+        score += (double)wcost[j] * mult;
+      }
+      if (score < best_score) {
+        best_score = score;
+        best_e = e;
+      }
+    }
+    if (best_e != spad) {
+      const int64_t old_stride = sstride;
+      sstride = (((int64_t)L + 2 * halo + 31) / 32) * 32 + best_e;
+      smem = (int64_t)C * sstride * 4;
+      for (auto& o : chan_off) o = (int)(o / old_stride * sstride);
+      b->sstride = (int)sstride;
+      b->smem_bytes = (int)smem;
+    }
+  }
   // RK_DUMP_CHUNKS=<path>: the chunk layout, one line per chunk (diagnostics)
   if (const char* dump = getenv("RK_DUMP_CHUNKS")) {
     if (FILE* f = fopen(dump, "a")) {
