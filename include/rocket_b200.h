@@ -85,6 +85,8 @@ typedef struct rk_bank_info_s {
                                series per 8-lane pass) in the fast-mode layout */
   int32_t n_eighth_chunks;  /* chunks laid out as eighth-warp chunks (eight
                                series per 4-lane pass) in the fast-mode layout */
+  int32_t n_runmajor_chunks; /* chunks whose run starts are dealt run-major
+                                (fewer shared-memory bank conflicts) */
 } rk_bank_info_t;
 
 /* ABI version (RK_ABI_VERSION) and the thread-local last error message. */

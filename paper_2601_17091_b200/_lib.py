@@ -80,6 +80,7 @@ class BankInfo(ctypes.Structure):
         ("n_paired_chunks", ctypes.c_int32),
         ("n_quarter_chunks", ctypes.c_int32),
         ("n_eighth_chunks", ctypes.c_int32),
+        ("n_runmajor_chunks", ctypes.c_int32),
     ]
 
 

@@ -60,7 +60,38 @@ struct HostChunk {
   rk::DevChunk dev;
   int64_t cost;       // instruction-slot estimate for one series
   bool tail = false;  // tail mode (the wide kernel's WChunk flag)
+  int amap = -1;      // run-major lane map: log2 g (transform_kernel.cuh run_positions), -1: residue-major
 };
+
+// Shared-memory wavefronts of a chunk's complete-run steps under either lane
+// map of run_positions (amap < 0: residue-major, else run-major with g =
+// 2^amap), summed over up to 24 steps spread over the chunk: the largest
+// number of a step's LANES run starts that share a bank (every window load
+// of the step replays that many times).
+int64_t lanemap_wavefronts(int d, int n, int R, int lanes, int amap) {
+  const int64_t RD = (int64_t)R * d, A = n / RD, full = A * d, nfull = full / lanes;
+  if (nfull == 0) return 0;
+  const int64_t samples = std::min<int64_t>(nfull, 24);
+  int64_t tot = 0;
+  for (int64_t k = 0; k < samples; ++k) {
+    const int64_t base = (nfull * k / samples) * lanes;
+    int cover[32] = {};
+    int mx = 0;
+    for (int l = 0; l < lanes; ++l) {
+      const int64_t i = base + l;
+      int64_t v;
+      if (amap < 0) {
+        v = (i / d) * RD + i % d;
+      } else {
+        const int64_t g = 1LL << amap, j = i >> amap;
+        v = (j % A) * RD + (j / A) * g + (i & (g - 1));
+      }
+      mx = std::max(mx, ++cover[v % 32]);
+    }
+    tot += mx;
+  }
+  return tot;
+}
 
 // Instruction-slot estimate of one chunk for one series at a given R
 // (positions per lane, stride = dilation), following the kernel's lane map
@@ -1048,6 +1079,7 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
   // model may end a chunk's R-position runs at the last complete run and
   // walk the remaining positions one per lane instead of as partial runs
   const bool tail_ok = wide_ok && !gmem && !getenv("RK_NO_TAIL");
+  const bool amap_ok = wide_ok && !gmem && !getenv("RK_NO_AMAP");
   const bool half_ok = half_margin > 0 && max_group >= 2 && wide_ok && !gmem && !getenv("RK_NO_HALF") &&
                        (int64_t)half_ctas * (2 * (int64_t)smem + 1024) <= (int64_t)st->smem_optin + 1024;
   // quarter-warp chunks (8 lanes per series, four series per pass): the
@@ -1178,6 +1210,17 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       if (lanes == 4) nck = nck == 0 ? 10 : 11;
       hc.cost = best;
       hc.tail = tail;
+      // lane map: run-major where it replays fewer shared-memory wavefronts
+      // (staged series, fixed channel slots; GMEM rows keep the residue-major
+      // map, whose consecutive lanes read consecutive addresses)
+      if (amap_ok && !sp && rk::nck_slots(nck) != 0 && rk::r_of(best_r) > 1) {
+        int kg = 0;
+        while (kg < 5 && (1 << (kg + 1)) <= lanes && d % (1 << (kg + 1)) == 0) ++kg;
+        const int R = rk::r_of(best_r);
+        const int64_t w_res = lanemap_wavefronts(d, n, R, lanes, -1);
+        const int64_t w_run = lanemap_wavefronts(d, n, R, lanes, kg);
+        if (w_run < w_res) hc.amap = kg;
+      }
       dc.cls = (kLenIdx[len] * rk::kNumR + best_r) * rk::kNumNck + nck;
       // weights: [slot][pair][tap][2]; a shorter kernel (ck < cc) is
       // centred in the LEN-tap frame with zero taps at both ends.
@@ -1267,9 +1310,9 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
       fprintf(f, "# bank K=%lld C=%d L=%d half_margin=%lld\n", (long long)K, C, L, (long long)half_margin);
       for (const auto& hc : b->chunks) {
         const rk::DevChunk& c = hc.dev;
-        fprintf(f, "len=%d R=%d nck=%d d=%d lo=%d n=%d nk=%d nc=%d cost=%lld tail=%d\n", c.len,
+        fprintf(f, "len=%d R=%d nck=%d d=%d lo=%d n=%d nk=%d nc=%d cost=%lld tail=%d amap=%d\n", c.len,
                 rk::r_of((c.cls / rk::kNumNck) % rk::kNumR), c.cls % rk::kNumNck, c.d, c.lo, c.n, c.nk, c.nc,
-                (long long)hc.cost, hc.tail ? 1 : 0);
+                (long long)hc.cost, hc.tail ? 1 : 0, hc.amap);
       }
       fclose(f);
     }
@@ -1356,7 +1399,9 @@ int bank_create_impl(int64_t K, int32_t C, int32_t L, const int32_t* lengths, co
               wc.ch[1] = c.nc;
             }
             wc.q32 = (short)c.q32;
-            wc.r32 = (short)(c.r32 | (b->chunks[i0 + j].tail ? rk::kTailFlag : 0));
+            const HostChunk& hcj = b->chunks[i0 + j];
+            wc.r32 = (short)(c.r32 | (hcj.tail ? rk::kTailFlag : 0) |
+                             (hcj.amap >= 0 ? rk::kAMapFlag | (hcj.amap << 8) : 0));
             wc.invd = c.invd;
             std::memcpy(raw + (size_t)j * sizeof(rk::WChunk), &wc, sizeof(wc));
             std::memcpy(raw + cursor, wpack.data() + c.wofs, wbytes);
@@ -1529,6 +1574,7 @@ int rk_bank_info(rk_bank_t b, rk_bank_info_t* info) {
     info->n_quarter_chunks += rk::nck_quarter(hc.dev.cls % rk::kNumNck) ? 1 : 0;
     info->n_eighth_chunks += rk::nck_eighth(hc.dev.cls % rk::kNumNck) ? 1 : 0;
     info->n_paired_chunks += rk::nck_sp(hc.dev.cls % rk::kNumNck) ? 1 : 0;
+    info->n_runmajor_chunks += hc.amap >= 0 ? 1 : 0;
   }
   if (b->wide_path)
     info->n_launches = (int32_t)b->wide_launches.size();

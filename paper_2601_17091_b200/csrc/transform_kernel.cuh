@@ -493,12 +493,22 @@ __device__ __forceinline__ void chunk_step(Pool<2 * P, MPV>& st, const float* co
 // v0 + r*d may pass n) through masked steps with clamped reads.
 // LANES = 16 / 8: a half / quarter warp walks one series (lane is the lane
 // in its group, q32 / r32 are LANES / d and LANES % d).
+//
+// Run-major map (amap = log2 g >= 0, chosen per chunk by the host where it
+// replays fewer shared-memory wavefronts): the complete-run starts are dealt
+// as i -> (sb, a, sl) with sl = i mod g fastest, then the run index a < A,
+// then the residue block sb (start s = sb*g + sl), g = the largest power of
+// two dividing d (<= LANES).  The LANES starts of a step are then LANES/g
+// consecutive runs of g residues: banks a*(R*d) + sl, distinct because R*d/g
+// is odd — where the residue-major map above puts d-position blocks R*d
+// apart and replays up to 5-way at d = 3, 5, 7, ... .  Both maps are a
+// mixed-radix counter (radix d / radix A) advanced by LANES per step.
 template <int LEN, int R, int P, int NC, bool EXACT, bool MPV = false, int LANES = 32>
 __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float* const (&chan)[NC],
                                               const float2 (&w)[NC][P][LEN], const float (&thr)[2 * P],
                                               const float2 (&init)[P], float2 one2, int lo, int n, int d, int q32,
                                               int r32, float invd, const float* nan_slot, int lane,
-                                              bool tail = false) {
+                                              bool tail = false, int amap = -1) {
   constexpr int kLog = LANES == 32 ? 5 : LANES == 16 ? 4 : LANES == 8 ? 3 : 2;
   const int RD = R * d;
   const int A = n / RD;          // complete runs per residue
@@ -508,32 +518,53 @@ __device__ __forceinline__ void run_positions(Pool<2 * P, MPV>& st, const float*
   // — a contiguous range — run below as an R = 1 map
   const int starts = (R > 1 && tail) ? full_starts : full_starts + min(d, rem);
   const int nfull = full_starts >> kLog;
-  // (a, s) = divmod(32*step + lane, d), advanced incrementally; the first
-  // divmod of lane < 32 is exact in float ((lane + 0.5) / d is never within
-  // 2^-20 of an integer)
-  int a = (int)((lane + 0.5f) * invd);
-  int s = lane - a * d;
-  int v0 = a * RD + s;
-  const int dv = q32 * RD + r32;
+  int t, v0, radix, tstep, vstep, vwrap;
+  if (R > 1 && amap >= 0 && A > 0) {
+    const int kg = min(amap, kLog), g = 1 << kg;
+    const int J = LANES >> kg, qa = J / A, ra = J - qa * A;  // runs per step = qa*A + ra
+    const int j = lane >> kg;
+    const int sb = j / A;
+    t = j - sb * A;  // run index a
+    v0 = t * RD + sb * g + (lane & (g - 1));
+    radix = A;
+    tstep = ra;
+    vstep = ra * RD + qa * g;
+    vwrap = g - A * RD;
+  } else {
+    // (a, s) = divmod(32*step + lane, d), advanced incrementally; the first
+    // divmod of lane < 32 is exact in float ((lane + 0.5) / d is never within
+    // 2^-20 of an integer)
+    const int a = (int)((lane + 0.5f) * invd);
+    t = lane - a * d;  // residue s
+    v0 = a * RD + t;
+    radix = d;
+    tstep = r32;
+    vstep = q32 * RD + r32;
+    vwrap = RD - d;
+  }
 #pragma unroll(kStepUnroll)
   for (int stp = 0; stp < nfull; ++stp) {
     chunk_step<LEN, R, P, NC, EXACT, false, MPV>(st, chan, w, thr, init, one2, lo + v0, d, n, nan_slot);
-    s += r32;
-    v0 += dv;
-    if (s >= d) {
-      s -= d;
-      v0 += RD - d;
+    t += tstep;
+    v0 += vstep;
+    if (t >= radix) {
+      t -= radix;
+      v0 += vwrap;
     }
   }
   for (int base = nfull << kLog; base < starts; base += LANES) {
-    const bool live = base + lane < starts;
-    chunk_step<LEN, R, P, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v0 : 0), d,
-                                           live ? n - v0 : 0, nan_slot);
-    s += r32;
-    v0 += dv;
-    if (s >= d) {
-      s -= d;
-      v0 += RD - d;
+    // starts past the complete runs (the partial run of each residue) sit at
+    // A*R*d + s in both maps
+    const int i = base + lane;
+    const bool live = i < starts;
+    const int v = i < full_starts ? v0 : A * RD + (i - full_starts);
+    chunk_step<LEN, R, P, NC, EXACT, true, MPV>(st, chan, w, thr, init, one2, lo + (live ? v : 0), d,
+                                           live ? n - v : 0, nan_slot);
+    t += tstep;
+    v0 += vstep;
+    if (t >= radix) {
+      t -= radix;
+      v0 += vwrap;
     }
   }
   if constexpr (R > 1) {
@@ -957,6 +988,11 @@ struct float4_t {  // host-side storage of the parameter blob
 // registers for the R = 1 path (kTailOK) ignore the flag and walk those
 // chunks as partial runs: the same outputs in another order.
 constexpr short kTailFlag = 0x4000;
+// WChunk.r32 bit 13: run-major lane map (run_positions amap), log2 g in bits
+// 8..10; bits 0..7 hold 32 % d (<= 32).
+constexpr short kAMapFlag = 0x2000;
+constexpr short kR32Mask = 0xFF;
+__device__ __forceinline__ int chunk_amap(int r32) { return (r32 & kAMapFlag) ? ((r32 >> 8) & 7) : -1; }
 struct __align__(16) WChunk {  // 80 bytes
   int d, lo, n, nk;
   int col[4];
@@ -1567,7 +1603,7 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             Pool<2, MPV> st;
             pool_init<2, EXACT, MPV>(st);
             run_positions_sp<LEN, R, NC, EXACT, MPV>(st, chan, ws, thr2, init2, one2, c.lo, c.n, c.d, c.q32,
-                                                     c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
+                                                     c.r32 & kR32Mask, c.invd, nanp, lane,
                                                      kTailOK && (c.r32 & kTailFlag) != 0);
             finish_chunk_sp<EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk, p.h.vec_out,
                                                 lane);
@@ -1600,7 +1636,8 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
             Pool<2 * P, MPV> st;
             pool_init<2 * P, EXACT, MPV>(st);
             run_positions<LEN, R, P, NC, EXACT, MPV, LG>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, qg, rg,
-                                                         c.invd, nanp, hl, kTailOK && (c.r32 & kTailFlag) != 0);
+                                                         c.invd, nanp, hl, kTailOK && (c.r32 & kTailFlag) != 0,
+                                                         chunk_amap(c.r32));
             float* orow0 = p.h.out + (series0 + si) * p.h.ld_out;
             float* orow = orow0;
 #pragma unroll
@@ -1620,8 +1657,8 @@ __global__ void __launch_bounds__(32 * kWideMaxWarps, 1) rocket_wide_kernel(cons
           Pool<2 * P, MPV> st;
           pool_init<2 * P, EXACT, MPV>(st);
           run_positions<LEN, R, P, NC, EXACT, MPV>(st, chan, w, thr, init, one2, c.lo, c.n, c.d, c.q32,
-                                                   c.r32 & (kTailFlag - 1), c.invd, nanp, lane,
-                                                   kTailOK && (c.r32 & kTailFlag) != 0);
+                                                   c.r32 & kR32Mask, c.invd, nanp, lane,
+                                                   kTailOK && (c.r32 & kTailFlag) != 0, chunk_amap(c.r32));
           finish_chunk<2 * P, EXACT, WChunk, MPV>(c, st, p.h.out + (series0 + si) * p.h.ld_out, p.h.fpk,
                                                   p.h.vec_out, lane);
           done += (unsigned long long)c.nk * (unsigned long long)c.n;

@@ -61,6 +61,7 @@ def test_benched_fast_path_full_size(name, n, c, l, stride, cuda_ready):
     if c == 1 and l <= 2048:
         # the layout the bench runs: half-warp chunks (two series per pass)
         assert db.info["n_half_chunks"] + db.info["n_quarter_chunks"] + db.info["n_eighth_chunks"] > 0
+    assert db.info["n_runmajor_chunks"] > 0  # both lane-map orders run in the timed layout
     x = torch.from_numpy(values).cuda()
     rows = np.arange(0, n, stride)
     rows[-1] = n - 1
@@ -227,3 +228,32 @@ def test_default_stream_ordering(cuda_ready):
         out = torch.full((len(values), bank.count * 2), float("nan"), device="cuda")
         db.transform_into(xd.data_ptr(), len(values), out.data_ptr(), out.shape[1], mode="exact")
         assert torch.equal(out, ref)  # default-stream comparison after the call
+
+
+def test_lane_map_orders_agree(monkeypatch, cuda_ready):
+    """The run-major lane map only reorders which lane walks which
+    run: PPV / MAX bytes equal the residue-major layout's (RK_NO_AMAP=1) in
+    both modes, and exact mode equals the oracle (3 channels, L = 2048: the
+    config-5 shape, whose d = 3, 5, 7, ... chunks take the run-major map)."""
+    import torch
+
+    from oracle.oracle import oracle_transform
+    from paper_2601_17091_b200.engine import DeviceBank
+
+    bank = generate_bank(2048, 3, 1500, GenOptions(seed=11))
+    n = 600
+    values = synth_random(n, 3, 2048, seed=12).values
+    x = torch.from_numpy(values).cuda()
+    db_run = DeviceBank(bank, 0)
+    monkeypatch.setenv("RK_NO_AMAP", "1")
+    db_res = DeviceBank(bank, 0)
+    assert db_run.info["n_runmajor_chunks"] > 0 and db_res.info["n_runmajor_chunks"] == 0
+    for mode in ("fast", "exact"):
+        a, ea = _device_transform(db_run, x, n, 2, mode)
+        b, eb = _device_transform(db_res, x, n, 2, mode)
+        assert ea == eb == expected_dot_products(bank, n)
+        assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes(), mode
+    rows = np.arange(0, n, 25)
+    assert a.cpu().numpy()[rows].tobytes() == oracle_transform(values[rows], bank).tobytes()
+    db_run.close()
+    db_res.close()
