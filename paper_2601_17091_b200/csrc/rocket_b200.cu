@@ -683,14 +683,28 @@ int launch_cellpair(DeviceState* st, const rk::CellArgs& a, size_t smem, cudaStr
   return RK_OK;
 }
 
+// Row stride of the cell kernels' own staging: 32-float rounding plus 12,
+// so the C channel rows start 12 banks apart in float32 and 24 in float64
+// (lanes of one warp read different channels at once).  The wide kernel's
+// pad (chosen for its lane groups, 16 at C = 3) puts float64 channel rows on
+// the same banks: config 5 float64 ran 32 % slower with it (pad sweep in
+// profiles/r02_cell_kernels.txt).  RK_CELL_PAD: another pad (floats,
+// multiple of 2; diagnostics).
+int64_t cell_sstride(rk_bank_t b) {
+  static const int pad = getenv("RK_CELL_PAD") ? std::max(0, atoi(getenv("RK_CELL_PAD")) / 2 * 2) : 12;
+  return (((int64_t)b->L + 2 * b->halo + 31) / 32) * 32 + pad;
+}
+
 template <typename T, bool MPV, bool GMEM>
 int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t stream, int* d_counters) {
-  const size_t smem = GMEM ? 0 : (size_t)b->C * b->sstride * sizeof(T);
+  const int64_t cs = GMEM ? b->sstride : cell_sstride(b);  // GMEM: the zero-haloed rows' stride
+  const size_t smem = GMEM ? 0 : (size_t)b->C * cs * sizeof(T);
   // the paired kernel when its two copies leave room for two CTAs per SM
-  const bool paired = !GMEM && !getenv("RK_NO_CELLPAIR") && 2 * (2 * smem + 1024) <= st->smem_optin + 1024;
+  const size_t psmem = 2 * smem + rk::kCellPairSlack * sizeof(T);  // two copies + dead-read slack
+  const bool paired = !GMEM && !getenv("RK_NO_CELLPAIR") && 2 * (psmem + 1024) <= st->smem_optin + 1024;
   RK_CUDA(cudaMemsetAsync(d_counters, 0, sizeof(int) * 3, stream));
   a.halo = b->halo;
-  a.sstride = b->sstride;
+  a.sstride = (int)cs;
   a.one = 1.0f;
   for (int li = 0; li < 3; ++li) {
     if (b->cell_len_end[li] <= b->cell_len_begin[li]) continue;
@@ -699,9 +713,9 @@ int launch_cellrows(rk_bank_t b, DeviceState* st, rk::CellArgs a, cudaStream_t s
     a.item_counter = d_counters + li;
     int rc;
     if (paired)
-      rc = li == 0 ? launch_cellpair<T, MPV, 7>(st, a, 2 * smem, stream)
-         : li == 1 ? launch_cellpair<T, MPV, 9>(st, a, 2 * smem, stream)
-                   : launch_cellpair<T, MPV, 11>(st, a, 2 * smem, stream);
+      rc = li == 0 ? launch_cellpair<T, MPV, 7>(st, a, psmem, stream)
+         : li == 1 ? launch_cellpair<T, MPV, 9>(st, a, psmem, stream)
+                   : launch_cellpair<T, MPV, 11>(st, a, psmem, stream);
     else
       rc = li == 0 ? launch_cellrow<T, MPV, 7, GMEM>(st, a, smem, stream)
          : li == 1 ? launch_cellrow<T, MPV, 9, GMEM>(st, a, smem, stream)
@@ -785,7 +799,7 @@ int launch_cells(rk_bank_t b, DeviceState* st, const void* d_x, int esz, int64_t
   a.l_series = b->L;
   a.n_channels = b->C;
   a.fpk = fpk;
-  const size_t staged = (size_t)b->C * b->sstride * esz;
+  const size_t staged = (size_t)b->C * cell_sstride(b) * esz;
   if (!getenv("RK_NO_CELLROW")) {
     if (staged + 1024 <= st->smem_optin) {
       if (esz == 8)

@@ -1290,6 +1290,9 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 // (row offset + j*d), so two base pointers per channel slot (even and odd
 // taps) replace any per-load selection.  MPV sums the positive outputs in
 // position order (t, then t + 1), as the reference does.
+#ifndef RK_CELLPAIR_NB32
+#define RK_CELLPAIR_NB32 8
+#endif
 template <typename T>
 struct Pair;
 template <>
@@ -1313,9 +1316,16 @@ __device__ __forceinline__ double2 pair_tap<double>(double2 acc, double w, doubl
   return make_double2(__dadd_rn(acc.x, __dmul_rn(w, x.x)), __dadd_rn(acc.y, __dmul_rn(w, x.y)));
 }
 
+// Positions per block: NB = 2 * NP pairs share each tap's address and
+// weight (float32: 8, one address per four 8-byte loads; float64: 4).
+template <typename T>
+__host__ __device__ constexpr int cellpair_nb() { return sizeof(T) == 4 ? RK_CELLPAIR_NB32 : 4; }
+constexpr int kCellPairSlack = 16;  // elements past the two copies (dead-position reads)
+
 template <typename T, bool MPV, int LEN>
 __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) {
   using V = typename Pair<T>::V;
+  constexpr int NB = cellpair_nb<T>(), NP = NB / 2;
   extern __shared__ __align__(16) unsigned char cell_smem[];
   T* copy0 = reinterpret_cast<T*>(cell_smem);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -1324,7 +1334,7 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
   __shared__ int s_item, s_next;
   if (tid == 0)
     RK_CHK_SET(copy0, nullptr, nullptr, nullptr, a.out, reinterpret_cast<T*>(a.out) + a.n_series * a.ld_out);
-  for (int k = tid; k < 2 * C * S; k += blockDim.x) copy0[k] = T(0);
+  for (int k = tid; k < 2 * C * S + kCellPairSlack; k += blockDim.x) copy0[k] = T(0);
   const int ngroups = (a.k_end - a.k_begin + 31) / 32;
   const T* wts = reinterpret_cast<const T*>(a.weights);
   const T* bis = reinterpret_cast<const T*>(a.biases);
@@ -1369,21 +1379,24 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
       const T* q01 = ((off0 + d) & 1) ? copy1 + off0 - 1 : copy0 + off0;
       int count = 0;
       T mx = T(-INFINITY), psum = T(0);
-      for (int t0 = 0; t0 < span; t0 += 4) {
+      for (int t0 = 0; t0 < span; t0 += NB) {
         // dead positions (t >= l_out) re-read the last live block; its
         // start is kept even (pairs (t, t + 1) stay aligned) and reads at
-        // most one position past l_out (inside the row's zero slack)
-        int tb = min(t0, max(lout - 4, 0));
+        // most one position past l_out (NB - 1 when l_out < NB; the
+        // allocation ends in kCellPairSlack zeroed elements)
+        int tb = min(t0, max(lout - NB, 0));
         tb += tb & 1;
-        V acc0, acc1;  // acc = +0, then RN(acc + RN(w*x)) tap by tap (engine.py:172-179)
-        acc0.x = acc0.y = acc1.x = acc1.y = T(0);
+        V acc[NP];  // acc = +0, then RN(acc + RN(w*x)) tap by tap (engine.py:172-179)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) acc[q].x = acc[q].y = T(0);
 #pragma unroll
         for (int j = 0; j < LEN; ++j) {
           const T* xp = ((j & 1) ? q01 : q00) + j * d + tb;
-          RK_CHK_READ(xp, 4 * (int)sizeof(T));
+          RK_CHK_READ(xp, NB * (int)sizeof(T));
           RK_CHK(((uintptr_t)xp & (2 * sizeof(T) - 1)) == 0);
-          acc0 = pair_tap<T>(acc0, w0[j], *reinterpret_cast<const V*>(xp), one2, false);
-          acc1 = pair_tap<T>(acc1, w0[j], *reinterpret_cast<const V*>(xp + 2), one2, false);
+#pragma unroll
+          for (int q = 0; q < NP; ++q)
+            acc[q] = pair_tap<T>(acc[q], w0[j], *reinterpret_cast<const V*>(xp + 2 * q), one2, false);
         }
         for (int c = 1; c < kd.nc; ++c) {
           const int off = __ldg(a.chidx + kd.choff + c) * S + H - kd.p;
@@ -1393,11 +1406,12 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
 #pragma unroll
           for (int j = 0; j < LEN; ++j) {
             const T* xp = ((j & 1) ? q1 : q0) + j * d + tb;
-            RK_CHK_READ(xp, 4 * (int)sizeof(T));
+            RK_CHK_READ(xp, NB * (int)sizeof(T));
             RK_CHK(((uintptr_t)xp & (2 * sizeof(T) - 1)) == 0);
             const T wj = wc[j];
-            acc0 = pair_tap<T>(acc0, wj, *reinterpret_cast<const V*>(xp), one2, false);
-            acc1 = pair_tap<T>(acc1, wj, *reinterpret_cast<const V*>(xp + 2), one2, false);
+#pragma unroll
+            for (int q = 0; q < NP; ++q)
+              acc[q] = pair_tap<T>(acc[q], wj, *reinterpret_cast<const V*>(xp + 2 * q), one2, false);
           }
         }
         auto pool = [&](T v) {
@@ -1410,17 +1424,20 @@ __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) 
           mx = v > mx ? v : mx;
         };
         const int shift = t0 - tb;
-        if (shift == 0 && t0 + 4 <= lout) {
-          pool(acc0.x);
-          pool(acc0.y);
-          pool(acc1.x);
-          pool(acc1.y);
+        if (shift == 0 && t0 + NB <= lout) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) {
+            pool(acc[q].x);
+            pool(acc[q].y);
+          }
         } else {
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < NB; ++b) {
             const int q = b + shift;
             if (t0 + b < lout) {
-              const T v = q == 0 ? acc0.x : q == 1 ? acc0.y : q == 2 ? acc1.x : acc1.y;
+              T v = acc[0].x;
+#pragma unroll
+              for (int r = 1; r < NB; ++r) v = q == r ? ((r & 1) ? acc[r / 2].y : acc[r / 2].x) : v;
               pool(v);
             }
           }
