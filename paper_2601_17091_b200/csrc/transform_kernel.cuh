@@ -1291,7 +1291,7 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 // taps) replace any per-load selection.  MPV sums the positive outputs in
 // position order (t, then t + 1), as the reference does.
 #ifndef RK_CELLPAIR_NB32
-#define RK_CELLPAIR_NB32 8
+#define RK_CELLPAIR_NB32 16
 #endif
 template <typename T>
 struct Pair;
@@ -1317,10 +1317,10 @@ __device__ __forceinline__ double2 pair_tap<double>(double2 acc, double w, doubl
 }
 
 // Positions per block: NB = 2 * NP pairs share each tap's address and
-// weight (float32: 8, one address per four 8-byte loads; float64: 4).
+// weight (float32: 16, one address per eight 8-byte loads; float64: 4).
 template <typename T>
 __host__ __device__ constexpr int cellpair_nb() { return sizeof(T) == 4 ? RK_CELLPAIR_NB32 : 4; }
-constexpr int kCellPairSlack = 16;  // elements past the two copies (dead-position reads)
+constexpr int kCellPairSlack = 32;  // elements past the two copies (dead-position reads reach <= NB past a row)
 
 template <typename T, bool MPV, int LEN>
 __global__ void __launch_bounds__(256) rocket_cellpair_kernel(const CellArgs a) {
