@@ -1293,6 +1293,9 @@ __global__ void __launch_bounds__(256) rocket_cellrow_kernel(const CellArgs a) {
 #ifndef RK_CELLPAIR_NB32
 #define RK_CELLPAIR_NB32 16
 #endif
+#ifndef RK_CELLPAIR_NB64
+#define RK_CELLPAIR_NB64 8
+#endif
 template <typename T>
 struct Pair;
 template <>
@@ -1317,9 +1320,9 @@ __device__ __forceinline__ double2 pair_tap<double>(double2 acc, double w, doubl
 }
 
 // Positions per block: NB = 2 * NP pairs share each tap's address and
-// weight (float32: 16, one address per eight 8-byte loads; float64: 4).
+// weight (float32: 16, one address per eight 8-byte loads; float64: 8).
 template <typename T>
-__host__ __device__ constexpr int cellpair_nb() { return sizeof(T) == 4 ? RK_CELLPAIR_NB32 : 4; }
+__host__ __device__ constexpr int cellpair_nb() { return sizeof(T) == 4 ? RK_CELLPAIR_NB32 : RK_CELLPAIR_NB64; }
 constexpr int kCellPairSlack = 32;  // elements past the two copies (dead-position reads reach <= NB past a row)
 
 template <typename T, bool MPV, int LEN>
