@@ -103,8 +103,9 @@ __host__ __device__ constexpr int nck_lanes(int nck) {
 // series per pass of a kind (1, 2, 4, 8)
 __host__ __device__ constexpr int nck_groups(int nck) { return 32 / nck_lanes(nck); }
 // largest R of the position-paired kinds (2R positions per lane: the pair
-// window and accumulators fit the ~80-register budget)
-__host__ __device__ constexpr int sp_rmax(int nc, int len) { return nc == 1 ? (len == 7 ? 9 : 7) : 5; }
+// window and accumulators fit the ~80-register budget; one slot walks its
+// window anti-diagonally, see chunk_step_sp)
+__host__ __device__ constexpr int sp_rmax(int nc, int len) { return nc == 1 ? 15 : 5; }
 __host__ __device__ constexpr int nck_full(int nck) {
   return (nck == 4 || nck == 8 || nck == 10) ? 0 : (nck == 5 || nck == 9 || nck == 11) ? 3 : nck;
 }
@@ -604,27 +605,43 @@ __device__ __forceinline__ void chunk_step_sp(Pool<2, MPV>& st, const float* con
   for (int s = 0; s < NC; ++s) {
     const float* pa = chan[s] + (u0a - C * d);
     const float* pb = chan[s] + (u0b - C * d);
-    float2 xp[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-      xp[q].x = sp_load<LEN>(pa, q, d, nlefta, nan_slot, MASKED);
-      xp[q].y = sp_load<LEN>(pb, q, d, nleftb, nan_slot, MASKED);
-    }
-#pragma unroll
-    for (int j = 0; j < LEN; ++j) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        // the weight as a broadcast scalar
-        const float2 w2 = make_float2(w[s][j], w[s][j]);
-        if (EXACT) {
-          if (s == 0 && j == 0)
-            acc[0][r] = fmul2(xp[r + j], w2);  // RN(w*x) == RN(+0 + RN(w*x))
-          else
-            acc[0][r] = ffma2(fmul2(xp[r + j], w2), one2, acc[0][r]);
-        } else {
-          acc[0][r] = ffma2(xp[r + j], w2, (s == 0 && j == 0) ? init : acc[0][r]);
-        }
+    auto tap = [&](int r, int j, float2 xq) {
+      // the weight as a broadcast scalar
+      const float2 w2 = make_float2(w[s][j], w[s][j]);
+      if (EXACT) {
+        if (s == 0 && j == 0)
+          acc[0][r] = fmul2(xq, w2);  // RN(w*x) == RN(+0 + RN(w*x))
+        else
+          acc[0][r] = ffma2(fmul2(xq, w2), one2, acc[0][r]);
+      } else {
+        acc[0][r] = ffma2(xq, w2, (s == 0 && j == 0) ? init : acc[0][r]);
       }
+    };
+    if constexpr (NC == 1) {
+      // anti-diagonal order: window entry q feeds taps j = q - r of the
+      // positions r it covers and is dead afterwards, so only a few entries
+      // are live at once (R up to 15 fits the registers); each output still
+      // adds its taps in order j = 0 .. LEN-1
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        float2 xq;
+        xq.x = sp_load<LEN>(pa, q, d, nlefta, nan_slot, MASKED);
+        xq.y = sp_load<LEN>(pb, q, d, nleftb, nan_slot, MASKED);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (q - r >= 0 && q - r < LEN) tap(r, q - r, xq);
+      }
+    } else {
+      float2 xp[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        xp[q].x = sp_load<LEN>(pa, q, d, nlefta, nan_slot, MASKED);
+        xp[q].y = sp_load<LEN>(pb, q, d, nleftb, nan_slot, MASKED);
+      }
+#pragma unroll
+      for (int j = 0; j < LEN; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) tap(r, j, xp[r + j]);
     }
   }
   // slot 0 pools run A's positions, slot 1 run B's (same kernel)
