@@ -1521,7 +1521,9 @@ int rk_bank_create(int64_t K, int32_t C, int32_t L, const int32_t* lengths, cons
   // the half-warp margin of the cost model, per mode (measured optima:
   // profiles/r01_half_margin_sweep.txt)
   const int64_t margin_fast = getenv("RK_HALF_MARGIN") ? atoi(getenv("RK_HALF_MARGIN")) : 101;
-  const int64_t margin_exact = getenv("RK_HALF_MARGIN_EXACT") ? atoi(getenv("RK_HALF_MARGIN_EXACT")) : 110;
+  // (exact: 103 after the run-major map and eighth-warp chunks; the sweep
+  // 103 / 105 / 107 / 110 is in profiles/r02_cta_sweep.txt)
+  const int64_t margin_exact = getenv("RK_HALF_MARGIN_EXACT") ? atoi(getenv("RK_HALF_MARGIN_EXACT")) : 103;
   int rc = bank_create_impl(K, C, L, lengths, dilations, paddings, biases, weights, woff, chidx, choff, chcnt, device,
                             margin_fast, 8, out);
   if (rc) return rc;
